@@ -1,0 +1,130 @@
+/* musr_b200.h -- C ABI of libmusr_b200.so, the DKS-style GPU layer for the
+ * uSR fit objective (chi2 / maximum log-likelihood) on NVIDIA B200 (sm_100a).
+ *
+ * Every entry point is plain C: int status (0 = MUSR_OK), no exceptions across
+ * the boundary, a per-handle last-error string.  A handle is driven by one
+ * host thread (the reference orchestration is single-threaded).
+ *
+ * Reference interfaces replaced (paths under the reference tree, pkg/src/blk):
+ *   musr_open / musr_open_sharded / musr_close
+ *       Backend construction + worker pool, backend.py:98-155 (DKS setAPI /
+ *       initDevice).  One handle = one GPU; sharded handles
+ *       additionally own an NCCL communicator (one rank per process).
+ *   musr_set_theory
+ *       theory.evaluate's bytecode interpreter, theory.py:409-464, replaced by
+ *       CUDA source generated from the AST (codegen.py) and compiled with
+ *       NVRTC for sm_100a (paper's runtime kernel generation).
+ *   musr_upload
+ *       Backend.allocate + DeviceBuffer.write, backend.py:44-76, 127-143, fed
+ *       with MusrDataset.counts / errors() / range_mask(), musr.py:66-101, and
+ *       the parameter-independent envelope exp(-t/tau_mu) of musr.py:162.
+ *   musr_eval
+ *       musr.chi2 / musr.mlh, musr.py:181-232, including model_expected
+ *       (musr.py:150-162) and Backend.map_reduce + pairwise_sum
+ *       (backend.py:79-95, 174-207).  Returns per-dataset sums, the left-folded
+ *       total (musr.py:190-201) and the MLH first non-positive bin per dataset.
+ *   musr_time_evals / musr_fp64_peak
+ *       measurement helpers for bench.py (no reference counterpart).
+ */
+#ifndef MUSR_B200_H
+#define MUSR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MUSR_OK 0
+#define MUSR_ERR_ARG 1      /* bad argument / state                       */
+#define MUSR_ERR_CUDA 2     /* CUDA runtime or driver failure            */
+#define MUSR_ERR_NVRTC 3    /* theory source failed to compile           */
+#define MUSR_ERR_NCCL 4     /* NCCL failure (sharded handles)            */
+#define MUSR_ERR_NOMEM 5    /* device or pinned allocation failed        */
+
+#define MUSR_KIND_CHI2 0
+#define MUSR_KIND_MLH 1
+
+#define MUSR_TILE_TERMS 2048  /* terms per CTA tile (layout granularity) */
+
+typedef struct musr_ctx musr_ctx;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int musr_version(void);
+
+/* Number of visible CUDA devices (0 when none). */
+int musr_device_count(int* n);
+
+/* Message of the last failure of a call that had no handle (musr_open*). */
+const char* musr_global_error(void);
+
+/* One GPU, no collective. */
+int musr_open(int device, musr_ctx** out);
+
+/* Sharded handle: this process is rank `rank` of `world`, each rank owning a
+ * disjoint set of datasets; results are combined with one fp64 ncclAllReduce
+ * per evaluation, captured in the evaluation's CUDA graph.  `nccl_lib` is the
+ * path of libnccl.so.2 (NULL: default dlopen search); `unique_id` is the
+ * 128-byte ncclUniqueId made by rank 0 with musr_nccl_unique_id. */
+int musr_nccl_unique_id(const char* nccl_lib, unsigned char out_id[128]);
+int musr_open_sharded(int device, int rank, int world, const char* nccl_lib,
+                      const unsigned char unique_id[128], musr_ctx** out);
+
+void musr_close(musr_ctx* ctx);
+const char* musr_last_error(const musr_ctx* ctx);
+
+/* Compile the theory fragment produced by codegen.lower() (defines MUSR_NU,
+ * musr_uniform, musr_theory) into the objective kernels.  Cached by source
+ * hash.  On MUSR_ERR_NVRTC the compiler log is copied into `log`. */
+int musr_set_theory(musr_ctx* ctx, const char* fragment, char* log, size_t log_cap);
+
+/* Compile-only check of a theory fragment (no device needed).  Returns the
+ * size of the sm_100a CUBIN NVRTC produced; the log as in musr_set_theory. */
+int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t* cubin_bytes);
+
+/* Upload the local datasets (copied; the device owns them afterwards).
+ *   n_global       datasets over all ranks (length of per-dataset outputs)
+ *   n_local        datasets owned by this handle
+ *   out_index[i]   global index of local dataset i
+ *   n_terms[i]     in-range bin count (> 0)
+ *   first_bin[i]   first in-range bin; t0_bin[i]; dt[i]
+ *   counts[i], errors[i], envelope[i]
+ *                  host arrays of n_terms[i] doubles starting at first_bin[i]
+ *                  (errors may be NULL: MLH-only handle)
+ *   n0_slot[i], nbkg_slot[i]   parameter indices (already wrapped)
+ *   maps           n_local * map_stride int32 (per-dataset map rows)
+ *   fvals          n_local * f_stride doubles (per-dataset function values)
+ *   p_capacity     maximum parameter-vector length accepted by musr_eval */
+int musr_upload(musr_ctx* ctx, int n_global, int n_local, const int32_t* out_index,
+                const int64_t* n_terms, const int64_t* first_bin, const int64_t* t0_bin,
+                const double* dt, const double* const* counts, const double* const* errors,
+                const double* const* envelope, const int32_t* n0_slot, const int32_t* nbkg_slot,
+                const int32_t* maps, int map_stride, const double* fvals, int f_stride,
+                int p_capacity);
+
+/* One synchronous objective evaluation: copy p (n_p <= p_capacity) to pinned
+ * staging, replay the CUDA graph (H2D p -> kernel -> [allreduce] -> D2H),
+ * wait, then fold.  per_dataset / first_bad_bin have n_global entries
+ * (first_bad_bin = -1: none).  total = left fold of per_dataset in global
+ * order (may be NULL). */
+int musr_eval(musr_ctx* ctx, int kind, const double* p, int n_p, double* per_dataset,
+              int64_t* first_bad_bin, double* total);
+
+/* Timing helpers (CUDA events on the handle's stream).
+ *   mode 0: `iters` back-to-back graph replays (full evaluation incl. H2D p and
+ *           D2H results, no host sync in between) -> *ms = total elapsed.
+ *   mode 1: `iters` kernel launches, each bracketed by its own events, with an
+ *           L2 flush before each when flush_l2 != 0 -> *ms = summed kernel time. */
+int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, double* ms);
+
+/* Number of CTAs (tiles) one evaluation launches on this handle. */
+int musr_tiles(const musr_ctx* ctx, int64_t* n_tiles);
+
+/* DFMA throughput probe: returns measured fp64 TFLOP/s (2 flops per DFMA). */
+int musr_fp64_peak(int device, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MUSR_B200_H */

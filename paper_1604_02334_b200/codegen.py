@@ -1,0 +1,378 @@
+"""Lower a theory AST to CUDA C++ for the NVRTC JIT (K3).
+
+The generated fragment defines two device functions that the kernel
+template in ``csrc/musr_kernel.cuh`` calls:
+
+``musr_uniform(P, M, F, U)``
+    evaluated once per histogram tile by one thread; computes every maximal
+    parameter-only ("uniform") subexpression into ``U[0..MUSR_NU)``.  This is
+    the hoisting of scalar numpy temporaries: in the reference interpreter
+    (theory.py:409-464) a subexpression that does not involve ``t`` stays an
+    ``np.float64`` scalar and is computed once per call.
+``musr_theory(t, U)``
+    the per-bin asymmetry A(t) for one bin, in registers.
+
+Arithmetic contract: every ``+ - * /`` is emitted as a
+round-to-nearest intrinsic (``__dadd_rn`` ...), which can never be contracted
+into an FMA, in exactly the association order numpy evaluates.  The builtin
+shapes are expanded with numpy's operand order (theory.py:62-80):
+
+* ``se(t,l)    = exp((-l) * t)``
+* ``ge(t,l,b)  = exp(-(npy_pow(l * t, b)))``
+* ``sg(t,s)    = exp(-0.5 * npy_pow(s * t, 2.0))``
+* ``stg(t,s)   = 1/3 + ((2/3) * (1 - st2)) * exp(-0.5 * st2)``, ``st2 = npy_pow(s*t, 2.0)``
+* ``tf(t,ph,nu)= cos(((2pi * nu) * t) + ((ph * pi) / 180))``
+
+``npy_pow`` follows numpy 2.x ``np.power`` (measured):
+with a bin-uniform exponent it short-cuts 2 -> x*x, 0.5 -> sqrt, -1 -> 1/x,
+1 -> x, 0 -> 1 and otherwise calls pow; a per-bin exponent always calls pow.
+
+Literal-only ``+ - * /`` subtrees are evaluated by the reference with Python
+floats (identical IEEE results, but ``x / 0.0`` raises ZeroDivisionError);
+they are folded here with Python floats and a zero divisor is recorded as a
+static error event in postfix order, so the objective raises exactly where
+the reference would.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Tuple
+
+from .theory import (
+    Binary,
+    Call,
+    Node,
+    Num,
+    SlotRef,
+    TheoryError,
+    TimeVar,
+    Unary,
+)
+
+__all__ = ["Lowered", "lower", "StaticEvent"]
+
+_TWO_PI = 2.0 * math.pi            # Python float product, == 2.0 * np.pi
+_PI = math.pi
+_ONE_THIRD = 1.0 / 3.0
+_TWO_THIRDS = 2.0 / 3.0
+
+
+@dataclass(frozen=True)
+class StaticEvent:
+    """A point in postfix order where the reference interpreter may raise:
+    ``kind`` is 'p' / 'f' (slot resolution, theory.py:425-435) or 'zdiv'
+    (Python float division by zero of two literals)."""
+
+    kind: str
+    slot: int = -1
+
+
+@dataclass
+class Lowered:
+    source: str                 # CUDA fragment (musr_uniform + musr_theory)
+    n_uniform: int              # MUSR_NU
+    uniform_exprs: List[str]    # readable form of each U slot (docs / debugging)
+    events: List[StaticEvent]   # postfix-ordered raise points
+    max_p_slot: int             # largest k in p[m[k]] (-1 if none)
+    max_f_slot: int             # largest k in f[m[k]] (-1 if none)
+    per_bin: bool               # does A depend on t at all
+
+
+# -- static events + literal folding on the user AST --------------------------
+
+class _ZeroDiv:
+    """Marker for a literal subtree whose evaluation raises."""
+
+
+def _events_and_fold(node: Node, events: List[StaticEvent]):
+    """Return (folded_node, pyfloat_value_or_None).  ``pyfloat`` is the Python
+    float the reference would hold for a literal-only subtree."""
+    if isinstance(node, Num):
+        return node, float(node.value)
+    if isinstance(node, TimeVar):
+        return node, None
+    if isinstance(node, SlotRef):
+        events.append(StaticEvent(node.array, node.slot))
+        return node, None
+    if isinstance(node, Unary):
+        inner, val = _events_and_fold(node.operand, events)
+        if isinstance(val, float):
+            return Num(-val), -val
+        return Unary("-", inner), None
+    if isinstance(node, Binary):
+        left, lv = _events_and_fold(node.left, events)
+        right, rv = _events_and_fold(node.right, events)
+        if node.op != "^" and isinstance(lv, float) and isinstance(rv, float):
+            if node.op == "+":
+                v = lv + rv
+            elif node.op == "-":
+                v = lv - rv
+            elif node.op == "*":
+                v = lv * rv
+            else:
+                if rv == 0.0:
+                    events.append(StaticEvent("zdiv"))
+                    return Binary(node.op, left, right), _ZeroDiv
+                v = lv / rv
+            return Num(v), v
+        return Binary(node.op, left, right), None
+    if isinstance(node, Call):
+        args = tuple(_events_and_fold(a, events)[0] for a in node.args)
+        return Call(node.name, args), None
+    raise TheoryError(f"unknown node {node!r}")
+
+
+# -- builtin expansion to primitives --------------------------------------------
+
+def _exp(x: Node) -> Node:
+    return Call("exp", (x,))
+
+
+def _desugar(node: Node) -> Node:
+    if isinstance(node, (Num, TimeVar, SlotRef)):
+        return node
+    if isinstance(node, Unary):
+        return Unary("-", _desugar(node.operand))
+    if isinstance(node, Binary):
+        return Binary(node.op, _desugar(node.left), _desugar(node.right))
+    if not isinstance(node, Call):
+        raise TheoryError(f"unknown node {node!r}")
+    a = tuple(_desugar(x) for x in node.args)
+    name = node.name
+    if name in ("exp", "log", "cos", "sin", "sqrt"):
+        return Call(name, a)
+    if name == "pow":
+        return Binary("^", a[0], a[1])
+    if name == "se":
+        t, lam = a
+        return _exp(Binary("*", Unary("-", lam), t))
+    if name == "ge":
+        t, lam, beta = a
+        return _exp(Unary("-", Binary("^", Binary("*", lam, t), beta)))
+    if name == "sg":
+        t, sigma = a
+        return _exp(Binary("*", Num(-0.5), Binary("^", Binary("*", sigma, t), Num(2.0))))
+    if name == "stg":
+        t, sigma = a
+        st2 = Binary("^", Binary("*", sigma, t), Num(2.0))
+        damp = _exp(Binary("*", Num(-0.5), st2))
+        return Binary(
+            "+",
+            Num(_ONE_THIRD),
+            Binary("*", Binary("*", Num(_TWO_THIRDS), Binary("-", Num(1.0), st2)), damp),
+        )
+    if name == "tf":
+        t, phi, nu = a
+        omega_t = Binary("*", Binary("*", Num(_TWO_PI), nu), t)
+        phase = Binary("/", Binary("*", phi, Num(_PI)), Num(180.0))
+        return Call("cos", (Binary("+", omega_t, phase),))
+    raise TheoryError(f"unknown function {name!r}")
+
+
+# -- emission ---------------------------------------------------------------------
+
+def _lit(v: float) -> str:
+    """Exact C++ double literal."""
+    if math.isnan(v):
+        return "__longlong_as_double(0x7ff8000000000000LL)"
+    if math.isinf(v):
+        return "__longlong_as_double(0x7ff0000000000000LL)" if v > 0 else \
+            "__longlong_as_double(0xfff0000000000000LL)"
+    if v == 0.0:
+        return "(-0.0)" if math.copysign(1.0, v) < 0 else "0.0"
+    return f"({v.hex()})"
+
+
+def _depends_on_t(node: Node, memo: Dict[Node, bool]) -> bool:
+    if node in memo:
+        return memo[node]
+    if isinstance(node, TimeVar):
+        r = True
+    elif isinstance(node, (Num, SlotRef)):
+        r = False
+    elif isinstance(node, Unary):
+        r = _depends_on_t(node.operand, memo)
+    elif isinstance(node, Binary):
+        r = _depends_on_t(node.left, memo) or _depends_on_t(node.right, memo)
+    else:
+        r = any(_depends_on_t(x, memo) for x in node.args)
+    memo[node] = r
+    return r
+
+
+_ARITH = {"+": "__dadd_rn", "-": "__dsub_rn", "*": "__dmul_rn", "/": "__ddiv_rn"}
+_FUNC = {
+    "exp": "exp",
+    "log": "log",
+    "cos": "cos",
+    "sin": "sin",
+    "sqrt": "__dsqrt_rn",
+}
+
+
+class _Emitter:
+    """SSA emitter with structural CSE (identical subtrees computed once,
+    which is bit-neutral)."""
+
+    def __init__(self, leaf):
+        self.lines: List[str] = []
+        self.names: Dict[Node, str] = {}
+        self.leaf = leaf          # callback for TimeVar/SlotRef/hoisted nodes
+        self.uniform_of = None    # callback: is the node bin-uniform?
+
+    def value(self, node: Node) -> str:
+        if isinstance(node, Num):
+            return _lit(float(node.value))
+        direct = self.leaf(node)
+        if direct is not None:
+            return direct
+        if node in self.names:
+            return self.names[node]
+        expr = self._expr(node)
+        name = f"v{len(self.names)}"
+        self.lines.append(f"  const double {name} = {expr};")
+        self.names[node] = name
+        return name
+
+    def _expr(self, node: Node) -> str:
+        if isinstance(node, Unary):
+            return f"(-{self.value(node.operand)})"
+        if isinstance(node, Binary):
+            if node.op == "^":
+                return self._pow(node)
+            return f"{_ARITH[node.op]}({self.value(node.left)}, {self.value(node.right)})"
+        if isinstance(node, Call):
+            return f"{_FUNC[node.name]}({self.value(node.args[0])})"
+        raise TheoryError(f"cannot emit {node!r}")
+
+    def _pow(self, node: Binary) -> str:
+        base = self.value(node.left)
+        ex = node.right
+        if isinstance(ex, Num):
+            e = float(ex.value)
+            if e == 2.0:
+                return f"musr_sq({base})"
+            if e == 0.5:
+                return f"__dsqrt_rn({base})"
+            if e == -1.0:
+                return f"__ddiv_rn(1.0, {base})"
+            if e == 1.0:
+                return base
+            if e == 0.0:
+                return "1.0"
+            return f"pow({base}, {_lit(e)})"
+        if self.uniform_of(ex):
+            return f"musr_npy_pow_u({base}, {self.value(ex)})"
+        return f"pow({base}, {self.value(ex)})"
+
+
+def lower(ast: Node) -> Lowered:
+    events: List[StaticEvent] = []
+    folded, pyval = _events_and_fold(ast, events)
+    prim = _desugar(folded)
+
+    memo: Dict[Node, bool] = {}
+    per_bin = _depends_on_t(prim, memo)
+
+    def uniform(n: Node) -> bool:
+        return not _depends_on_t(n, memo)
+
+    # 1) collect maximal uniform, non-literal subtrees (hoisted to U)
+    hoisted: Dict[Node, int] = {}
+    order: List[Node] = []
+
+    def collect(n: Node) -> None:
+        if isinstance(n, Num):
+            return
+        if uniform(n):
+            if n not in hoisted:
+                hoisted[n] = len(order)
+                order.append(n)
+            return
+        if isinstance(n, Unary):
+            collect(n.operand)
+        elif isinstance(n, Binary):
+            collect(n.left)
+            collect(n.right)
+        elif isinstance(n, Call):
+            for x in n.args:
+                collect(x)
+
+    collect(prim)
+    if not per_bin and not isinstance(prim, Num) and not order:
+        order.append(prim)
+        hoisted[prim] = 0
+
+    # 2) uniform prologue: slot loads through the per-histogram map row
+    def uleaf(n: Node) -> Optional[str]:
+        if isinstance(n, SlotRef):
+            arr = "P" if n.array == "p" else "F"
+            return f"{arr}[M[{n.slot}]]"
+        if isinstance(n, TimeVar):
+            raise TheoryError("internal: t inside a uniform subtree")
+        return None
+
+    ue = _Emitter(uleaf)
+    ue.uniform_of = lambda n: True
+    u_lines: List[str] = []
+    for i, n in enumerate(order):
+        ue.lines = []
+        val = ue.value(n)
+        u_lines.extend(ue.lines)
+        u_lines.append(f"  U[{i}] = {val};")
+
+    # 3) per-bin body
+    def bleaf(n: Node) -> Optional[str]:
+        if isinstance(n, TimeVar):
+            return "t"
+        if n in hoisted:
+            return f"U[{hoisted[n]}]"
+        return None
+
+    be = _Emitter(bleaf)
+    be.uniform_of = uniform
+    result = be.value(prim)
+
+    nu = len(order)
+    src: List[str] = []
+    src.append(f"#define MUSR_NU {max(nu, 1)}")
+    src.append("__device__ __forceinline__ void musr_uniform(const double* __restrict__ P, "
+               "const int* __restrict__ M, const double* __restrict__ F, double* __restrict__ U) {")
+    src.append("  (void)P; (void)M; (void)F;")
+    src.extend(u_lines)
+    if nu == 0:
+        src.append("  U[0] = 0.0;")
+    src.append("}")
+    src.append("__device__ __forceinline__ double musr_theory(const double t, const double* __restrict__ U) {")
+    src.append("  (void)t; (void)U;")
+    src.extend(be.lines)
+    src.append(f"  return {result};")
+    src.append("}")
+
+    p_slots = [e.slot for e in events if e.kind == "p"]
+    f_slots = [e.slot for e in events if e.kind == "f"]
+    return Lowered(
+        source="\n".join(src) + "\n",
+        n_uniform=max(nu, 1),
+        uniform_exprs=[_readable(n) for n in order],
+        events=events,
+        max_p_slot=max(p_slots, default=-1),
+        max_f_slot=max(f_slots, default=-1),
+        per_bin=per_bin,
+    )
+
+
+def _readable(n: Node) -> str:
+    if isinstance(n, Num):
+        return repr(n.value)
+    if isinstance(n, TimeVar):
+        return "t"
+    if isinstance(n, SlotRef):
+        return f"{n.array}[m[{n.slot}]]"
+    if isinstance(n, Unary):
+        return f"(-{_readable(n.operand)})"
+    if isinstance(n, Binary):
+        return f"({_readable(n.left)} {n.op} {_readable(n.right)})"
+    return f"{n.name}({', '.join(_readable(a) for a in n.args)})"

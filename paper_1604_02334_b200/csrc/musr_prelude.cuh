@@ -1,0 +1,18 @@
+// musr_prelude.cuh -- device helpers available to the generated theory
+// fragment (codegen.py).  Included before the fragment; musr_kernel.cuh after.
+#ifndef MUSR_PRELUDE_CUH
+#define MUSR_PRELUDE_CUH
+
+__device__ __forceinline__ double musr_sq(double x) { return __dmul_rn(x, x); }
+
+// np.power with a bin-uniform exponent (numpy 2.x fast paths, measured).
+__device__ __forceinline__ double musr_npy_pow_u(double x, double b) {
+  if (b == 2.0) return __dmul_rn(x, x);
+  if (b == 0.5) return __dsqrt_rn(x);
+  if (b == -1.0) return __ddiv_rn(1.0, x);
+  if (b == 1.0) return x;
+  if (b == 0.0) return 1.0;
+  return pow(x, b);
+}
+
+#endif  // MUSR_PRELUDE_CUH

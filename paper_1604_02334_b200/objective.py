@@ -1,0 +1,445 @@
+"""GPU objective sessions: the drop-in replacement for musr.chi2 / musr.mlh.
+
+A *session* is one (datasets, theory, tau_mu, parameter-vector length) problem
+resident on one GPU (or one shard of it on one rank).  Building a session:
+
+1. lowers the theory AST to CUDA (codegen.py) and JIT-compiles it (NVRTC);
+2. computes, once, the parameter-independent per-bin streams with the same
+   numpy expressions the reference evaluates on every call, so they are
+   bit-identical to it:
+     * fit interval [first, last] from ``range_mask``      musr.py:98-101
+     * errors ``max(1, sqrt(d))``                           musr.py:95-96
+     * envelope ``exp(-t / tau_mu)``                        musr.py:162
+   and uploads counts/errors/envelope of the in-range bins (``musr_upload``);
+3. resolves, per dataset, every error the reference interpreter would raise
+   for this parameter-vector length (empty range, map coverage / range,
+   literal division by zero, N0/Nbkg index) in the reference's order.
+
+An evaluation copies p to pinned memory and replays the CUDA graph
+(``musr_eval``); the host only folds the per-dataset sums in dataset order
+and maps the first failing dataset to the reference exception.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from collections import OrderedDict
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from .codegen import Lowered, lower
+from .theory import (
+    Binary,
+    Call,
+    EvalError,
+    Num,
+    SlotRef,
+    TheoryError,
+    TimeVar,
+    Unary,
+    parse,
+)
+
+__all__ = ["DeviceBackend", "Session", "shard_assignment", "session_for", "ErrorTypes"]
+
+
+# -- exception classes used for raised errors ----------------------------------------
+
+@dataclass
+class ErrorTypes:
+    """Exception classes raised by the objective.  Default: this package's own
+    mirrors; ``install()`` swaps in the host package's (e.g. the reference's
+    ``blk.musr.MusrError`` / ``blk.theory.EvalError``) so callers catching those
+    keep working."""
+
+    musr: type = None
+    eval: type = EvalError
+
+
+ERRORS = ErrorTypes()
+
+
+# -- backend: device selection / sharding ------------------------------------------
+
+@dataclass(frozen=True)
+class DeviceBackend:
+    """Execution backend for the GPU objective (the DKS device selection).
+
+    ``world == 1``: one GPU, no collective.  ``world > 1``: this process is
+    rank ``rank``; datasets are split into contiguous, bin-balanced shards and
+    the per-dataset results are combined by one fp64 ncclAllReduce per
+    evaluation inside the CUDA graph.  Every rank must call the objective with
+    the same datasets and p (SPMD), like the reference's single caller.
+    """
+
+    device: int = 0
+    rank: int = 0
+    world: int = 1
+    nccl_id: Optional[bytes] = field(default=None, repr=False)
+    worker_count: int = 1          # accepted for signature compatibility
+
+    @property
+    def kind(self) -> str:
+        return f"B200(device={self.device})" if self.world == 1 else \
+            f"B200(device={self.device}, rank={self.rank}/{self.world})"
+
+    @classmethod
+    def from_torch_distributed(cls, device: Optional[int] = None) -> "DeviceBackend":
+        """Build a sharded backend from an initialised torch.distributed group
+        (plumbing only: the NCCL unique id is broadcast with it)."""
+        import torch.distributed as dist  # plumbing, not the product
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        if device is None:
+            import os
+
+            device = int(os.environ.get("LOCAL_RANK", rank))
+        if world == 1:
+            return cls(device=device)
+        holder = [None]
+        if rank == 0:
+            holder[0] = new_nccl_id()
+        dist.broadcast_object_list(holder, src=0)
+        return cls(device=device, rank=rank, world=world, nccl_id=holder[0])
+
+
+def new_nccl_id() -> bytes:
+    lib = _lib.load()
+    buf = C.create_string_buffer(128)
+    path = _lib.nccl_library_path()
+    _lib.check(lib.musr_nccl_unique_id(path.encode() if path else None, buf), None,
+               "musr_nccl_unique_id")
+    return buf.raw
+
+
+def shard_assignment(n_terms: Sequence[int], world: int) -> List[int]:
+    """Rank owning each dataset: contiguous blocks balanced by in-range bins.
+    Dataset j goes to floor(world * midpoint_j / total), midpoint_j being the
+    cumulative bin count at the centre of dataset j."""
+    n = [int(x) for x in n_terms]
+    total = sum(n)
+    if world <= 1 or total == 0:
+        return [0] * len(n)
+    out = []
+    acc = 0
+    for x in n:
+        mid2 = 2 * acc + x      # 2 * midpoint, integers only
+        out.append(min(world - 1, (world * mid2) // (2 * total)))
+        acc += x
+    return out
+
+
+# -- per-dataset preparation --------------------------------------------------------
+
+def _adopt_ast(expr):
+    """Accept a TheoryExpr from this package or from the reference package:
+    rebuild its AST with this package's node classes (same names/fields)."""
+    def conv(n):
+        name = type(n).__name__
+        if name == "Num":
+            return Num(float(n.value))
+        if name == "TimeVar":
+            return TimeVar()
+        if name == "SlotRef":
+            return SlotRef(str(n.array), int(n.slot))
+        if name == "Unary":
+            return Unary(n.op, conv(n.operand))
+        if name == "Binary":
+            return Binary(n.op, conv(n.left), conv(n.right))
+        if name == "Call":
+            return Call(n.name, tuple(conv(a) for a in n.args))
+        raise TypeError(name)
+
+    ast = getattr(expr, "ast", None)
+    if ast is not None:
+        try:
+            return conv(ast)
+        except (TypeError, AttributeError):
+            pass
+    return parse(expr.source).ast
+
+
+_LOWER_CACHE: Dict[object, Lowered] = {}
+
+
+def _lowered(ast) -> Lowered:
+    low = _LOWER_CACHE.get(ast)
+    if low is None:
+        low = lower(ast)
+        _LOWER_CACHE[ast] = low
+    return low
+
+
+@dataclass
+class _Prepared:
+    index: int
+    detector: int
+    error: Optional[BaseException]        # static error for this p length
+    first: int = 0
+    n_terms: int = 0
+    counts: Optional[np.ndarray] = None
+    errors: Optional[np.ndarray] = None
+    envelope: Optional[np.ndarray] = None
+
+
+def _static_error(ds, low: Lowered, n_p: int, musr_error: type, eval_error: type):
+    """The exception the reference would raise for this dataset *before* the
+    MLH positivity check, or None (musr.py:191-197, theory.py:425-435)."""
+    m = tuple(ds.binding.map)
+    n_f = len(ds.binding.function_values)
+    for ev in low.events:
+        if ev.kind == "zdiv":
+            return ZeroDivisionError("float division by zero")
+        k = ev.slot
+        if k >= len(m):
+            return eval_error(f"slot {k} not covered by map of length {len(m)}")
+        j = m[k]
+        size = n_p if ev.kind == "p" else n_f
+        if j >= size:
+            return eval_error(
+                f"map entry m[{k}]={j} out of range for {ev.kind!r} array of length {size}"
+            )
+    for slot in (ds.n0_slot, ds.nbkg_slot):
+        if not -n_p <= int(slot) < n_p:
+            return IndexError(f"index {int(slot)} is out of bounds for axis 0 with size {n_p}")
+    return None
+
+
+def _prepare(j: int, ds, low: Lowered, tau_mu: float, n_p: int, musr_error, eval_error,
+             need_streams: bool) -> _Prepared:
+    counts = np.asarray(ds.counts)
+    # musr.py:92-93 / 98-101, evaluated exactly as the reference does
+    t = (np.arange(len(counts)) - ds.t0_bin) * ds.dt
+    lo, hi = ds.fit_range if ds.fit_range is not None else (0.0, np.inf)
+    mask = (t >= max(lo, 0.0)) & (t <= hi)
+    if not mask.any():
+        return _Prepared(j, ds.detector_index,
+                         musr_error(f"detector {ds.detector_index}: empty fit range"))
+    err = _static_error(ds, low, n_p, musr_error, eval_error)
+    if err is not None:
+        return _Prepared(j, ds.detector_index, err)
+    first = int(np.argmax(mask))
+    last = len(mask) - 1 - int(np.argmax(mask[::-1]))
+    if not mask[first:last + 1].all():   # t is monotone for dt > 0, so never
+        raise ValueError(f"detector {ds.detector_index}: fit range is not contiguous")
+    prep = _Prepared(j, ds.detector_index, None, first, last - first + 1)
+    if need_streams:
+        sl = slice(first, last + 1)
+        d = counts.astype(np.float64, copy=False)
+        prep.counts = np.ascontiguousarray(d[sl])
+        prep.errors = np.ascontiguousarray(np.maximum(1.0, np.sqrt(d))[sl])     # musr.py:95-96
+        prep.envelope = np.ascontiguousarray(np.exp(-t / tau_mu)[sl])           # musr.py:162
+    return prep
+
+
+def _fresh(exc: BaseException) -> BaseException:
+    """A new instance of a cached static error (clean traceback per raise)."""
+    try:
+        return type(exc)(*exc.args)
+    except Exception:
+        return exc
+
+
+# -- the session ------------------------------------------------------------------------
+
+class Session:
+    """One resident objective problem (see module docstring)."""
+
+    def __init__(self, datasets: Sequence, expr, tau_mu: float, n_p: int,
+                 backend: Optional[DeviceBackend] = None, musr_error: type = None,
+                 eval_error: type = None):
+        self.backend = backend or DeviceBackend()
+        self.n_p = int(n_p)
+        self.n_global = len(datasets)
+        self.tau_mu = float(tau_mu)
+        musr_error = musr_error or ERRORS.musr
+        eval_error = eval_error or ERRORS.eval
+        self.lowered = _lowered(_adopt_ast(expr))
+        self._handle = None
+        lib = _lib.load()
+
+        be = self.backend
+        # static analysis for all datasets (every rank knows every dataset's error)
+        preps = [_prepare(j, ds, self.lowered, self.tau_mu, self.n_p, musr_error, eval_error,
+                          need_streams=False) for j, ds in enumerate(datasets)]
+        self.static_errors: List[Tuple[int, BaseException]] = [
+            (p.index, p.error) for p in preps if p.error is not None
+        ]
+        live = [p for p in preps if p.error is None]
+        owner = shard_assignment([p.n_terms for p in live], be.world)
+        mine = [p for p, r in zip(live, owner) if r == be.rank]
+        self.local_indices = [p.index for p in mine]
+        self.local_terms = sum(p.n_terms for p in mine)
+        self.total_terms = sum(p.n_terms for p in live)
+        streams = [_prepare(p.index, datasets[p.index], self.lowered, self.tau_mu, self.n_p,
+                            musr_error, eval_error, need_streams=True) for p in mine]
+
+        # per-dataset map / f rows (padded; only validated slots are dereferenced)
+        map_stride = max([1, self.lowered.max_p_slot + 1, self.lowered.max_f_slot + 1] +
+                         [len(datasets[p.index].binding.map) for p in mine])
+        f_stride = max([1] + [len(datasets[p.index].binding.function_values) for p in mine])
+        nl = len(mine)
+        maps = np.zeros((max(nl, 1), map_stride), dtype=np.int32)
+        fvals = np.zeros((max(nl, 1), f_stride), dtype=np.float64)
+        n0 = np.zeros(max(nl, 1), dtype=np.int32)
+        nbkg = np.zeros(max(nl, 1), dtype=np.int32)
+        for i, p in enumerate(mine):
+            ds = datasets[p.index]
+            m = ds.binding.map
+            maps[i, :len(m)] = m
+            fv = ds.binding.function_values
+            fvals[i, :len(fv)] = fv
+            n0[i] = int(ds.n0_slot) % self.n_p       # numpy negative-index wrap
+            nbkg[i] = int(ds.nbkg_slot) % self.n_p
+        p_capacity = max(1, self.n_p)
+
+        handle = C.c_void_p()
+        if be.world == 1:
+            _lib.check(lib.musr_open(be.device, C.byref(handle)), None, "musr_open")
+        else:
+            if be.nccl_id is None or len(be.nccl_id) != 128:
+                raise ValueError("sharded DeviceBackend needs a 128-byte nccl_id")
+            path = _lib.nccl_library_path()
+            _lib.check(lib.musr_open_sharded(be.device, be.rank, be.world,
+                                             path.encode() if path else None,
+                                             be.nccl_id, C.byref(handle)),
+                       None, "musr_open_sharded")
+        self._handle = handle
+        self._lib = lib
+        log = C.create_string_buffer(1 << 16)
+        _lib.check(lib.musr_set_theory(handle, self.lowered.source.encode(), log, len(log)),
+                   handle, "musr_set_theory")
+
+        def arr(a, ct):
+            return np.ascontiguousarray(a).ctypes.data_as(C.POINTER(ct))
+
+        out_index = np.array([p.index for p in mine] or [0], dtype=np.int32)
+        n_terms = np.array([p.n_terms for p in mine] or [0], dtype=np.int64)
+        first_bin = np.array([p.first for p in mine] or [0], dtype=np.int64)
+        t0 = np.array([int(datasets[p.index].t0_bin) for p in mine] or [0], dtype=np.int64)
+        dts = np.array([float(datasets[p.index].dt) for p in mine] or [0.0], dtype=np.float64)
+        keep = [s.counts for s in streams] + [s.errors for s in streams] + \
+            [s.envelope for s in streams]
+        cptr = (C.c_void_p * max(nl, 1))(*[s.counts.ctypes.data for s in streams])
+        eptr = (C.c_void_p * max(nl, 1))(*[s.errors.ctypes.data for s in streams])
+        vptr = (C.c_void_p * max(nl, 1))(*[s.envelope.ctypes.data for s in streams])
+        rc = lib.musr_upload(
+            handle, self.n_global, nl, arr(out_index, C.c_int32), arr(n_terms, C.c_int64),
+            arr(first_bin, C.c_int64), arr(t0, C.c_int64), arr(dts, C.c_double),
+            C.cast(cptr, C.POINTER(C.c_void_p)), C.cast(eptr, C.POINTER(C.c_void_p)),
+            C.cast(vptr, C.POINTER(C.c_void_p)), arr(n0, C.c_int32), arr(nbkg, C.c_int32),
+            arr(maps, C.c_int32), map_stride, arr(fvals, C.c_double), f_stride, p_capacity)
+        del keep
+        _lib.check(rc, handle, "musr_upload")
+
+        self._p = np.zeros(p_capacity, dtype=np.float64)
+        self._sums = np.zeros(self.n_global, dtype=np.float64)
+        self._bad = np.zeros(self.n_global, dtype=np.int64)
+        self._total = C.c_double(0.0)
+        self._args_out = (self._sums.ctypes.data_as(C.POINTER(C.c_double)),
+                          self._bad.ctypes.data_as(C.POINTER(C.c_int64)),
+                          C.byref(self._total))
+        self.first_static = self.static_errors[0] if self.static_errors else None
+
+    # -- evaluation ---------------------------------------------------------------
+    def run(self, kind: int, p: np.ndarray) -> None:
+        """Launch one evaluation; results in self._sums / self._bad / self._total."""
+        rc = self._lib.musr_eval(self._handle, kind, p.ctypes.data_as(C.POINTER(C.c_double)),
+                                 len(p), *self._args_out)
+        if rc != _lib.MUSR_OK:
+            _lib.check(rc, self._handle, "musr_eval")
+
+    def evaluate(self, kind: int, p, datasets=None, musr_error: type = None) -> float:
+        """Objective value with the reference's error semantics."""
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        if len(p) != self.n_p:
+            raise ValueError("parameter vector length differs from the session's")
+        static = self.first_static
+        if static is not None and (static[0] == 0 or self.total_terms == 0):
+            raise _fresh(static[1])
+        self.run(kind, p)
+        if kind == _lib.KIND_MLH:
+            bad = np.flatnonzero(self._bad >= 0)
+            if len(bad) and (static is None or bad[0] < static[0]):
+                j = int(bad[0])
+                det = self._detectors[j] if self._detectors is not None else j
+                raise (musr_error or ERRORS.musr)(
+                    f"detector {det}: model is non-positive at bin {int(self._bad[j])}")
+        if static is not None:
+            raise _fresh(static[1])
+        return self._total.value
+
+    _detectors: Optional[List[int]] = None
+
+    def per_dataset(self) -> np.ndarray:
+        return self._sums.copy()
+
+    def time_evals(self, kind: int, iters: int, mode: int, flush_l2: bool = False) -> float:
+        ms = C.c_double(0.0)
+        _lib.check(self._lib.musr_time_evals(self._handle, kind, iters, mode, int(flush_l2),
+                                             C.byref(ms)), self._handle, "musr_time_evals")
+        return ms.value
+
+    def n_tiles(self) -> int:
+        n = C.c_int64(0)
+        self._lib.musr_tiles(self._handle, C.byref(n))
+        return n.value
+
+    def close(self) -> None:
+        if self._handle:
+            self._lib.musr_close(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# -- session cache for the drop-in functions ---------------------------------------
+
+_CACHE: "OrderedDict[tuple, Tuple[Session, list]]" = OrderedDict()
+_CACHE_MAX = 4
+_CACHE_LOCK = threading.Lock()
+
+
+def _signature(datasets, expr, tau_mu, n_p, backend) -> tuple:
+    parts = []
+    for ds in datasets:
+        parts.append((id(ds), id(ds.counts), ds.fit_range, ds.dt, ds.t0_bin, ds.binding,
+                      ds.n0_slot, ds.nbkg_slot, ds.detector_index))
+    return (tuple(parts), id(expr), getattr(expr, "source", None), tau_mu, n_p, backend)
+
+
+def session_for(datasets, expr, tau_mu: float, n_p: int, backend: DeviceBackend) -> Session:
+    """Return the cached session for this problem, building it on first use.
+    Datasets are treated as immutable while cached; replacing a
+    dataset's counts array, fit range or binding invalidates the entry."""
+    key = _signature(datasets, expr, tau_mu, n_p, backend)
+    with _CACHE_LOCK:
+        hit = _CACHE.get(key)
+        if hit is not None:
+            _CACHE.move_to_end(key)
+            return hit[0]
+    sess = Session(datasets, expr, tau_mu, n_p, backend)
+    sess._detectors = [int(ds.detector_index) for ds in datasets]
+    pin = [(ds, ds.counts) for ds in datasets] + [expr]   # keep ids alive while cached
+    with _CACHE_LOCK:
+        _CACHE[key] = (sess, pin)
+        _CACHE.move_to_end(key)
+        while len(_CACHE) > _CACHE_MAX:
+            _, (old, _) = _CACHE.popitem(last=False)
+            old.close()
+    return sess
+
+
+def clear_cache() -> None:
+    with _CACHE_LOCK:
+        while _CACHE:
+            _, (old, _) = _CACHE.popitem(last=False)
+            old.close()

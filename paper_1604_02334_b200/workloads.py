@@ -1,0 +1,114 @@
+"""Named benchmark / parity workloads, built from the mirror
+types.  Counts are synthetic Poisson draws around the configured model; the
+expected counts are computed once on the GPU-free host with numpy purely to
+synthesise input data (not part of any measured path).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from .musr import GAMMA_MU, TAU_MU_US, MusrDataset, default_phases
+from .theory import TheoryBinding, TheoryExpr, parse
+
+K_MHZ_PER_T = GAMMA_MU / (2.0 * np.pi)
+EQ6 = f"p[m[0]] * sg(t, p[m[1]]) * tf(t, p[m[2]] + f[m[4]], {K_MHZ_PER_T!r} * p[m[3]])"
+
+
+@dataclass
+class Workload:
+    name: str
+    expr: TheoryExpr
+    params: np.ndarray
+    bindings: List[TheoryBinding]
+    n0_slots: List[int]
+    nbkg_slots: List[int]
+    nbins: int
+    seed: int
+
+    @property
+    def dt(self) -> float:
+        return 10.0 / self.nbins
+
+    @property
+    def n_hist(self) -> int:
+        return len(self.bindings)
+
+
+def c1(nbins: int = 1 << 16) -> Workload:
+    return Workload("C1", parse("p[m[0]] * se(t, p[m[1]]) * tf(t, p[m[2]], p[m[3]])"),
+                    np.array([0.25, 0.5, 30.0, 1.5, 1000.0, 10.0]),
+                    [TheoryBinding(map=(0, 1, 2, 3))], [4], [5], nbins, 1234)
+
+
+def c2(n_hist: int = 8, nbins: int = 1 << 20) -> Workload:
+    # shared sigma, phi0, B; per-detector A0_j, N0_j, Nbkg_j (3 + 3*n params)
+    p = [0.2, 0.0, 0.05]
+    bindings, n0s, nbs = [], [], []
+    for j in range(n_hist):
+        a, n0, nb = len(p), len(p) + 1, len(p) + 2
+        p += [0.25, 1000.0, 10.0]
+        bindings.append(TheoryBinding(map=(a, 0, 1, 2, 0), function_values=(45.0 * j,)))
+        n0s.append(n0)
+        nbs.append(nb)
+    return Workload("C2", parse(EQ6), np.array(p), bindings, n0s, nbs, nbins, 2)
+
+
+def c3(n_hist: int = 16, nbins: int = 1 << 20) -> Workload:
+    return Workload("C3", parse("p[m[0]] * stg(t, p[m[1]]) * se(t, p[m[2]]) + "
+                                "p[m[3]] * ge(t, p[m[4]], p[m[5]])"),
+                    np.array([0.2, 0.3, 0.1, 0.05, 0.5, 1.5, 1000.0, 10.0]),
+                    [TheoryBinding(map=(0, 1, 2, 3, 4, 5)) for _ in range(n_hist)],
+                    [6] * n_hist, [7] * n_hist, nbins, 3)
+
+
+def c4(n_hist: int = 64, nbins: int = 1 << 22) -> Workload:
+    return Workload("C4", parse(EQ6), np.array([0.25, 0.2, 0.0, 0.05, 1000.0, 10.0]),
+                    [TheoryBinding(map=(0, 1, 2, 3, 0), function_values=(float(ph),))
+                     for ph in default_phases(n_hist)],
+                    [4] * n_hist, [5] * n_hist, nbins, 4)
+
+
+def c5(n_hist: int = 8, nbins: int = 1 << 20) -> Workload:
+    w = c4(n_hist, nbins)
+    w.name, w.seed = "C5", 5
+    w.bindings = [TheoryBinding(map=(0, 1, 2, 3, 0), function_values=(45.0 * j,))
+                  for j in range(n_hist)]
+    return w
+
+
+WORKLOADS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
+
+
+def synthesize(w: Workload, model: Optional[Callable] = None) -> List[MusrDataset]:
+    """Poisson counts around the workload model.  ``model(ds, expr, p)`` gives
+    expected counts; the default is a direct numpy formula for the fixed
+    workload theories (input synthesis only)."""
+    rng = np.random.default_rng(w.seed)
+    out = []
+    for j, b in enumerate(w.bindings):
+        ds = MusrDataset(j, np.zeros(w.nbins, dtype=np.int64), w.dt, 0, b,
+                         w.n0_slots[j], w.nbkg_slots[j])
+        lam = (model or _numpy_model)(ds, w, w.params)
+        ds.counts = rng.poisson(np.maximum(lam, 0.0)).astype(np.float64)
+        out.append(ds)
+    return out
+
+
+def _numpy_model(ds, w: Workload, p) -> np.ndarray:
+    t = ds.times()
+    m = ds.binding.map
+    if w.name in ("C2", "C4", "C5"):
+        ph = p[m[2]] + ds.binding.function_values[m[4]]
+        a = p[m[0]] * np.exp(-0.5 * (p[m[1]] * t) ** 2) * np.cos(
+            2 * np.pi * K_MHZ_PER_T * p[m[3]] * t + ph * np.pi / 180.0)
+    elif w.name == "C1":
+        a = p[m[0]] * np.exp(-p[m[1]] * t) * np.cos(2 * np.pi * p[m[3]] * t + p[m[2]] * np.pi / 180)
+    else:
+        s2 = (p[m[1]] * t) ** 2
+        a = (p[m[0]] * (1 / 3 + 2 / 3 * (1 - s2) * np.exp(-0.5 * s2)) * np.exp(-p[m[2]] * t)
+             + p[m[3]] * np.exp(-(p[m[4]] * t) ** p[m[5]]))
+    return p[ds.n0_slot] * np.exp(-t / TAU_MU_US) * (1.0 + a) + p[ds.nbkg_slot]
