@@ -46,7 +46,7 @@ extern "C" {
 #define MUSR_KIND_CHI2 0
 #define MUSR_KIND_MLH 1
 
-#define MUSR_TILE_TERMS 2048  /* terms per CTA tile (layout granularity) */
+#define MUSR_ROUND_TERMS 256  /* terms per warp round; tiles are 1-8 rounds */
 
 typedef struct musr_ctx musr_ctx;
 
@@ -118,8 +118,13 @@ int musr_eval(musr_ctx* ctx, int kind, const double* p, int n_p, double* per_dat
  *           L2 flush before each when flush_l2 != 0 -> *ms = summed kernel time. */
 int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, double* ms);
 
-/* Number of CTAs (tiles) one evaluation launches on this handle. */
+/* Number of tiles (units of 256*R terms) one evaluation processes here. */
 int musr_tiles(const musr_ctx* ctx, int64_t* n_tiles);
+
+/* Developer timeline (handles opened with MUSR_TRACE=1 in the environment):
+ * copies 4 %globaltimer stamps per CTA of the last objective launch of `kind`
+ * (CTA start, first tile landed, stage-2 done, producer exit; 0 = not reached). */
+int musr_debug_trace(musr_ctx* ctx, int kind, uint64_t* out, int cap, int* n_ctas);
 
 /* DFMA throughput probe: returns measured fp64 TFLOP/s (2 flops per DFMA). */
 int musr_fp64_peak(int device, double* tflops);

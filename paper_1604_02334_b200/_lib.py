@@ -17,7 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libmusr_b200.so"
 MUSR_OK = 0
 KIND_CHI2 = 0
 KIND_MLH = 1
-TILE_TERMS = 2048
+ROUND_TERMS = 256
 
 _DP = C.POINTER(C.c_double)
 _I64P = C.POINTER(C.c_int64)
@@ -50,6 +50,8 @@ SIGNATURES = [
     ("musr_time_evals", C.c_int,
      [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     ("musr_tiles", C.c_int, [C.c_void_p, _I64P]),
+    ("musr_debug_trace", C.c_int,
+     [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]),
     ("musr_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double)]),
 ]
 

@@ -9,8 +9,13 @@ template in ``csrc/musr_kernel.cuh`` calls:
     the hoisting of scalar numpy temporaries: in the reference interpreter
     (theory.py:409-464) a subexpression that does not involve ``t`` stays an
     ``np.float64`` scalar and is computed once per call.
-``musr_theory(t, U)``
-    the per-bin asymmetry A(t) for one bin, in registers.
+``musr_theory(t, U, ok)``
+    the per-bin asymmetry A(t) for one bin, in registers, with the branch-free
+    fast transcendentals of ``csrc/musr_math.cuh``; clears ``ok`` when an
+    argument leaves their fast domain.
+``musr_theory_exact(t, U)``
+    the same expression with the exact-domain functions; the kernel recomputes
+    a thread's bins with it when ``ok`` was cleared (deferred exception check).
 
 Arithmetic contract: every ``+ - * /`` is emitted as a
 round-to-nearest intrinsic (``__dadd_rn`` ...), which can never be contracted
@@ -203,12 +208,17 @@ def _depends_on_t(node: Node, memo: Dict[Node, bool]) -> bool:
 
 
 _ARITH = {"+": "__dadd_rn", "-": "__dsub_rn", "*": "__dmul_rn", "/": "__ddiv_rn"}
-_FUNC = {
-    "exp": "exp",
+_FUNC_EXACT = {             # uniform prologue and the rare exact fallback
+    "exp": "musr_exp",      # csrc/musr_math.cuh: <= 1 ulp, libdevice beyond |x| > 708
     "log": "log",
-    "cos": "cos",
-    "sin": "sin",
+    "cos": "musr_cos",      # abs. error <= 2.5e-16 for |x| < 2^20, libdevice beyond
+    "sin": "musr_sin",
     "sqrt": "__dsqrt_rn",
+}
+_FUNC_FAST = {              # hot loop: branch-free, clear `ok` outside the fast domain
+    "exp": "musr_exp_fast",
+    "cos": "musr_cos_fast",
+    "sin": "musr_sin_fast",
 }
 
 
@@ -216,11 +226,12 @@ class _Emitter:
     """SSA emitter with structural CSE (identical subtrees computed once,
     which is bit-neutral)."""
 
-    def __init__(self, leaf):
+    def __init__(self, leaf, fast: bool = False):
         self.lines: List[str] = []
         self.names: Dict[Node, str] = {}
         self.leaf = leaf          # callback for TimeVar/SlotRef/hoisted nodes
         self.uniform_of = None    # callback: is the node bin-uniform?
+        self.fast = fast          # emit *_fast(x, ok) variants
 
     def value(self, node: Node) -> str:
         if isinstance(node, Num):
@@ -244,7 +255,10 @@ class _Emitter:
                 return self._pow(node)
             return f"{_ARITH[node.op]}({self.value(node.left)}, {self.value(node.right)})"
         if isinstance(node, Call):
-            return f"{_FUNC[node.name]}({self.value(node.args[0])})"
+            arg = self.value(node.args[0])
+            if self.fast and node.name in _FUNC_FAST:
+                return f"{_FUNC_FAST[node.name]}({arg}, ok)"
+            return f"{_FUNC_EXACT[node.name]}({arg})"
         raise TheoryError(f"cannot emit {node!r}")
 
     def _pow(self, node: Binary) -> str:
@@ -323,7 +337,10 @@ def lower(ast: Node) -> Lowered:
         u_lines.extend(ue.lines)
         u_lines.append(f"  U[{i}] = {val};")
 
-    # 3) per-bin body
+    # 3) per-bin body: a branch-free fast variant that clears `ok` when an
+    #    argument leaves the fast domain, and the exact variant the kernel
+    #    falls back to (reading the uniform row from memory, so the hot loop's
+    #    registers are never forced to local memory).
     def bleaf(n: Node) -> Optional[str]:
         if isinstance(n, TimeVar):
             return "t"
@@ -331,9 +348,12 @@ def lower(ast: Node) -> Lowered:
             return f"U[{hoisted[n]}]"
         return None
 
-    be = _Emitter(bleaf)
-    be.uniform_of = uniform
-    result = be.value(prim)
+    bodies = {}
+    for fast in (True, False):
+        be = _Emitter(bleaf, fast=fast)
+        be.uniform_of = uniform
+        result = be.value(prim)
+        bodies[fast] = (be.lines, result)
 
     nu = len(order)
     src: List[str] = []
@@ -345,10 +365,17 @@ def lower(ast: Node) -> Lowered:
     if nu == 0:
         src.append("  U[0] = 0.0;")
     src.append("}")
-    src.append("__device__ __forceinline__ double musr_theory(const double t, const double* __restrict__ U) {")
+    src.append("__device__ __forceinline__ double musr_theory(const double t, "
+               "const double* __restrict__ U, bool& ok) {")
+    src.append("  (void)t; (void)U; (void)ok;")
+    src.extend(bodies[True][0])
+    src.append(f"  return {bodies[True][1]};")
+    src.append("}")
+    src.append("__device__ __noinline__ double musr_theory_exact(const double t, "
+               "const double* __restrict__ U) {")
     src.append("  (void)t; (void)U;")
-    src.extend(be.lines)
-    src.append(f"  return {result};")
+    src.extend(bodies[False][0])
+    src.append(f"  return {bodies[False][1]};")
     src.append("}")
 
     p_slots = [e.slot for e in events if e.kind == "p"]

@@ -20,6 +20,8 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -31,7 +33,6 @@
 #include "musr_embedded.inc"  // kMusrLayoutSrc, kMusrPreludeSrc, kMusrKernelSrc (generated at build time)
 
 static_assert(sizeof(MusrHist) == 64, "MusrHist layout");
-static_assert(MUSR_TILE_TERMS == 2048, "tile size must match musr_kernel.cuh");
 
 namespace {
 
@@ -89,6 +90,8 @@ struct DriverApi {
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, unsigned, CUstream, void**, void**) = nullptr;
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
 };
 std::mutex g_drv_mu;
 DriverApi g_drv;
@@ -103,6 +106,9 @@ bool load_driver(std::string* err) {
       {"cuModuleUnload", (void**)&d.ModuleUnload},
       {"cuLaunchKernel", (void**)&d.LaunchKernel},
       {"cuGetErrorString", (void**)&d.GetErrorString},
+      {"cuOccupancyMaxActiveBlocksPerMultiprocessor",
+       (void**)&d.OccupancyMaxActiveBlocksPerMultiprocessor},
+      {"cuFuncSetAttribute", (void**)&d.FuncSetAttribute},
   };
   for (auto& s : syms) {
     cudaDriverEntryPointQueryResult q;
@@ -146,8 +152,20 @@ struct musr_ctx {
 
   // theory module
   CUmodule mod = nullptr;
-  CUfunction fn[2] = {nullptr, nullptr};
+  CUfunction fn[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [kind][fmt]
+  CUfunction fn_utab = nullptr;
   bool have_theory = false;
+  int n_uniform = 1;            // MUSR_NU of the loaded theory
+  int sms = 0;                  // multiprocessors on the device
+  int per_thread = 8;           // MUSR_PT: terms per consumer thread; tile = 256 * per_thread
+  int stages = 2;               // MUSR_STAGES: TMA pipeline depth
+  int min_blocks = 2;           // MUSR_MIN_BLOCKS: register budget target
+  double* utab = nullptr;       // uniform table (sized at graph build)
+  size_t utab_rows = 0;
+  unsigned long long* trace = nullptr;  // MUSR_TRACE=1: per-CTA timeline
+  unsigned grid[2] = {0, 0};    // persistent grid per kind
+  size_t dyn_smem[2] = {0, 0};  // dynamic shared memory per kind
+  int per_thread_data = 8;      // per_thread the uploaded layout was padded for
 
   // data
   bool have_data = false;
@@ -155,9 +173,13 @@ struct musr_ctx {
   int n_global = 0, n_local = 0;
   int64_t n_tiles = 0;
   int p_capacity = 0;
-  double* d = nullptr;
+  void* d = nullptr;            // fp64 or fp32 (c32 format)
   double* e = nullptr;
+  double* rcp = nullptr;
   double* env = nullptr;
+  double2* table = nullptr;
+  int table_size = 0;
+  int fmt = 0;                  // 0: f64 streams, 1: c32 (fp32 counts + err/rcp table)
   int* tile_hist = nullptr;
   MusrHist* hist = nullptr;
   double* P = nullptr;
@@ -183,7 +205,41 @@ struct musr_ctx {
   size_t flush_bytes = 0;
 };
 
+// Tile layout of one stream (musr_kernel.cuh): tiles of 256*pt terms; inside a
+// tile the 16-byte group k*256 + t holds thread t's elements g*k .. g*k+g-1
+// (g = 16 / element size), so consumer reads are conflict-free LDS.128.
+// mode 0: fp64 copy, 1: fp32 (exact for the c32 format), 2: fp64 reciprocal
+// (__drcp_rn == IEEE 1.0/x, the Markstein divisor of musr_div_y).
+__global__ void musr_layout_stream(const double* __restrict__ src, void* __restrict__ dst,
+                                   size_t terms, unsigned pt, int mode) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= terms) return;
+  const size_t tile_terms = 256u * pt;
+  const size_t tile = i / tile_terms;
+  const unsigned r = (unsigned)(i - tile * tile_terms);
+  const unsigned g = (mode == 1) ? 4u : 2u;
+  const unsigned grp = r / g, e = r - grp * g, k = grp >> 8, t = grp & 255u;
+  const double v = src[tile * tile_terms + (size_t)t * pt + g * k + e];
+  if (mode == 1)
+    static_cast<float*>(dst)[i] = (float)v;
+  else
+    static_cast<double*>(dst)[i] = (mode == 2) ? __drcp_rn(v) : v;
+}
+
+// c32 table: {max(1, sqrt(k)), 1 / that}, both correctly rounded like numpy's
+// np.maximum(1.0, np.sqrt(d)) and 1.0 / err.
+__global__ void musr_build_table(double2* table, int n) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double s = __dsqrt_rn((double)k);
+  const double e = s < 1.0 ? 1.0 : s;
+  table[k] = make_double2(e, __drcp_rn(e));
+}
+
 namespace {
+
+constexpr int kThreads = 288;          // MUSR_THREADS: 8 consumer warps + 1 producer warp
+constexpr int kConsumers = 256;        // MUSR_CTHREADS
 
 int set_err(musr_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg; else g_error = msg;
@@ -217,11 +273,14 @@ void free_graphs(musr_ctx* c) {
 
 void free_data(musr_ctx* c) {
   free_graphs(c);
-  void* dev[] = {c->d, c->e, c->env, c->tile_hist, c->hist, c->P, c->maps, c->fvals,
-                 c->partial, c->count, c->bad, c->out_send, c->out_recv};
+  void* dev[] = {c->d, c->e, c->rcp, c->env, c->table, c->tile_hist, c->hist, c->P, c->maps,
+                 c->fvals, c->partial, c->count, c->bad, c->out_send, c->out_recv, c->utab};
   for (void* p : dev)
     if (p) cudaFree(p);
-  c->d = c->e = c->env = nullptr;
+  c->d = nullptr;
+  c->e = c->rcp = c->env = nullptr;
+  c->table = nullptr;
+  c->table_size = 0;
   c->tile_hist = nullptr;
   c->hist = nullptr;
   c->P = nullptr;
@@ -231,6 +290,8 @@ void free_data(musr_ctx* c) {
   c->count = nullptr;
   c->bad = nullptr;
   c->out_send = c->out_recv = nullptr;
+  c->utab = nullptr;
+  c->utab_rows = 0;
   if (c->h_p) cudaFreeHost(c->h_p);
   if (c->h_out) cudaFreeHost(c->h_out);
   c->h_p = c->h_out = nullptr;
@@ -241,8 +302,11 @@ void free_data(musr_ctx* c) {
 MusrArgs make_args(const musr_ctx* c) {
   MusrArgs a;
   a.d = c->d;
-  a.e = c->have_errors ? c->e : c->d;
+  a.e = c->e;
+  a.rcp = c->rcp;
   a.env = c->env;
+  a.table = c->table;
+  a.table_size = c->table_size;
   a.tile_hist = c->tile_hist;
   a.hist = c->hist;
   a.P = c->P;
@@ -252,22 +316,76 @@ MusrArgs make_args(const musr_ctx* c) {
   a.count = c->count;
   a.bad = c->bad;
   a.out = c->out_send;
+  a.utab = c->utab;
+  a.trace = c->trace;
+  a.n_tiles = (int)c->n_tiles;
   a.n_global = c->n_global;
+  a.n_local = c->n_local;
   return a;
 }
 
-int launch_kernel(musr_ctx* c, int kind) {
+// The evaluation's kernels: uniform table, then the objective tiles.
+int launch_kernels(musr_ctx* c, int kind, bool with_table) {
   if (c->n_tiles == 0) return MUSR_OK;  // rank without datasets
   MusrArgs a = make_args(c);
   void* params[] = {&a};
-  CU_TRY(c, g_drv.LaunchKernel(c->fn[kind], (unsigned)c->n_tiles, 1, 1, 256, 1, 1, 0,
-                           (CUstream)c->stream, params, nullptr));
+  if (with_table)
+    CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1,
+                                 1, 0, (CUstream)c->stream, params, nullptr));
+  CU_TRY(c, g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, kThreads, 1, 1,
+                               (unsigned)c->dyn_smem[kind], (CUstream)c->stream, params, nullptr));
+  return MUSR_OK;
+}
+
+constexpr int kMaxStaged = 64;          // MUSR_MAX_STAGED
+constexpr int kTableMax = 4096;         // c32 format: counts must be integers < this
+
+// Persistent grid and dynamic shared memory per objective kind.
+int plan_launch(musr_ctx* c) {
+  const size_t tile = (size_t)kConsumers * c->per_thread;  // terms per tile
+  for (int kind = 0; kind < 2; ++kind) {
+    // MusrGeom in musr_kernel.cuh: d | env | err | rcp
+    size_t stage = tile * (c->fmt ? 4 : 8) + tile * 8;
+    if (kind == 0 && c->fmt == 0) stage += 2 * tile * 8;
+    size_t smem = (size_t)c->stages * stage;
+    if (kind == 0 && c->fmt == 1) smem += (size_t)c->table_size * 16;
+    if (c->n_local <= kMaxStaged)
+      smem += (size_t)c->n_local * (c->n_uniform + 2) * sizeof(double);
+    c->dyn_smem[kind] = smem;
+    CUfunction fn = c->fn[kind][c->fmt];
+    CU_TRY(c, g_drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                     (int)smem));
+    int occ = 0;
+    CU_TRY(c, g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
+    if (occ < 1) return set_err(c, MUSR_ERR_CUDA, "objective kernel does not fit on an SM");
+    const int64_t cap = (int64_t)c->sms * occ;
+    c->grid[kind] = (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, cap));
+  }
+  if (std::getenv("MUSR_TRACE") && !c->trace) {
+    CUDA_TRY(c, cudaMalloc(&c->trace, (size_t)c->sms * 8 * 4 * sizeof(unsigned long long)));
+    CUDA_TRY(c, cudaMemset(c->trace, 0, (size_t)c->sms * 8 * 4 * sizeof(unsigned long long)));
+  }
+  return MUSR_OK;
+}
+
+// Uniform table sized for the loaded theory and data.
+int ensure_utab(musr_ctx* c) {
+  const size_t rows = (size_t)std::max(1, c->n_local) * (size_t)(c->n_uniform + 2);
+  if (c->utab && c->utab_rows >= rows) return MUSR_OK;
+  if (c->utab) cudaFree(c->utab);
+  c->utab = nullptr;
+  CUDA_TRY(c, cudaMalloc(&c->utab, rows * sizeof(double)));
+  CUDA_TRY(c, cudaMemset(c->utab, 0, rows * sizeof(double)));
+  c->utab_rows = rows;
   return MUSR_OK;
 }
 
 int build_graphs(musr_ctx* c) {
   free_graphs(c);
   if (!c->have_theory || !c->have_data) return MUSR_OK;
+  int prc = ensure_utab(c);
+  if (prc == MUSR_OK) prc = plan_launch(c);
+  if (prc != MUSR_OK) return prc;
   for (int kind = 0; kind < 2; ++kind) {
     if (kind == 0 && !c->have_errors) continue;
     cudaGraph_t g = nullptr;
@@ -277,9 +395,14 @@ int build_graphs(musr_ctx* c) {
     MusrArgs a = make_args(c);
     void* params[] = {&a};
     CUresult lr = CUDA_SUCCESS;
-    if (c->n_tiles > 0)
-      lr = g_drv.LaunchKernel(c->fn[kind], (unsigned)c->n_tiles, 1, 1, 256, 1, 1, 0,
-                          (CUstream)c->stream, params, nullptr);
+    if (c->n_tiles > 0) {
+      lr = g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1, 1,
+                              0, (CUstream)c->stream, params, nullptr);
+      if (lr == CUDA_SUCCESS)
+        lr = g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, kThreads, 1, 1,
+                                (unsigned)c->dyn_smem[kind], (CUstream)c->stream, params,
+                                nullptr);
+    }
     int nr = 0;
     if (c->comm)
       nr = g_nccl.AllReduce(c->out_send, c->out_recv, (size_t)2 * c->n_global, kNcclFloat64,
@@ -323,6 +446,12 @@ int open_common(int device, musr_ctx** out, musr_ctx** made) {
   if (!load_driver(&derr)) return set_err(nullptr, MUSR_ERR_CUDA, derr);
   musr_ctx* c = new musr_ctx();
   c->device = device;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (c->sms < 1) c->sms = 1;
+  // tuning overrides (defaults are the measured best on B200)
+  if (const char* v = std::getenv("MUSR_PT")) c->per_thread = std::atoi(v) == 4 ? 4 : 8;
+  if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(4, std::atoi(v)));
+  if (const char* v = std::getenv("MUSR_MIN_BLOCKS")) c->min_blocks = std::max(1, std::min(4, std::atoi(v)));
   ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (ce != cudaSuccess) {
     delete c;
@@ -397,6 +526,7 @@ void musr_close(musr_ctx* c) {
   if (c->mod) g_drv.ModuleUnload(c->mod);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   if (c->flush) cudaFree(c->flush);
+  if (c->trace) cudaFree(c->trace);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -408,14 +538,33 @@ const char* musr_last_error(const musr_ctx* c) { return c ? c->err.c_str() : g_e
 namespace {
 
 // NVRTC: (prelude + fragment + kernel template) -> sm_100a CUBIN, cached by source.
-int jit_compile(musr_ctx* c, const char* fragment, char* log, size_t log_cap, std::string* cubin) {
+int jit_compile(musr_ctx* c, int per_thread, int stages, int min_blocks, const char* fragment,
+                char* log, size_t log_cap, std::string* cubin) {
   std::string src = std::string("#include \"musr_prelude.cuh\"\n// generated theory\n") + fragment +
                     "\n#include \"musr_kernel.cuh\"\n";
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17",
-                        "-lineinfo", "--prec-div=true", "--prec-sqrt=true", "--ftz=false"};
-  const int n_opts = sizeof(opts) / sizeof(opts[0]);
+  std::vector<std::string> opt_s = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17",
+                                    "-lineinfo", "--prec-div=true", "--prec-sqrt=true",
+                                    "--ftz=false", "-DMUSR_PT=" + std::to_string(per_thread),
+                                    "-DMUSR_STAGES=" + std::to_string(stages),
+                                    "-DMUSR_MIN_BLOCKS=" + std::to_string(min_blocks)};
+  if (std::getenv("MUSR_TRACE")) opt_s.push_back("-DMUSR_TRACE");
+  // tuning hook: extra NVRTC options (e.g. "-DMUSR_PREFETCH=0 -DMUSR_MIN_BLOCKS=3")
+  if (const char* extra = std::getenv("MUSR_NVRTC_OPTS")) {
+    std::string s(extra), tok;
+    for (size_t i = 0; i <= s.size(); ++i) {
+      if (i == s.size() || s[i] == ' ') {
+        if (!tok.empty()) opt_s.push_back(tok);
+        tok.clear();
+      } else {
+        tok += s[i];
+      }
+    }
+  }
+  std::vector<const char*> opts;
+  for (auto& o : opt_s) opts.push_back(o.c_str());
+  const int n_opts = (int)opts.size();
   std::string key = src;
-  for (const char* o : opts) key += std::string("\n//opt ") + o;
+  for (auto& o : opt_s) key += "\n//opt " + o;
   {
     std::lock_guard<std::mutex> lk(g_jit_mu);
     auto it = g_cubin_cache.find(key);
@@ -425,14 +574,16 @@ int jit_compile(musr_ctx* c, const char* fragment, char* log, size_t log_cap, st
       return MUSR_OK;
     }
   }
-  const char* hdr_src[] = {kMusrLayoutSrc, kMusrPreludeSrc, kMusrKernelSrc};
-  const char* hdr_name[] = {"musr_layout.h", "musr_prelude.cuh", "musr_kernel.cuh"};
+  const char* hdr_src[] = {kMusrLayoutSrc, kMusrMathSrc, kMusrPreludeSrc, kMusrKernelSrc};
+  const char* hdr_name[] = {"musr_layout.h", "musr_math.cuh", "musr_prelude.cuh",
+                            "musr_kernel.cuh"};
+  const int n_hdr = sizeof(hdr_src) / sizeof(hdr_src[0]);
   nvrtcProgram prog;
   std::string pname = fmt("musr_theory_%016llx.cu", (unsigned long long)fnv1a(key));
-  nvrtcResult nr = nvrtcCreateProgram(&prog, src.c_str(), pname.c_str(), 3, hdr_src, hdr_name);
+  nvrtcResult nr = nvrtcCreateProgram(&prog, src.c_str(), pname.c_str(), n_hdr, hdr_src, hdr_name);
   if (nr != NVRTC_SUCCESS)
     return set_err(c, MUSR_ERR_NVRTC, fmt("nvrtcCreateProgram: %s", nvrtcGetErrorString(nr)));
-  nr = nvrtcCompileProgram(prog, n_opts, opts);
+  nr = nvrtcCompileProgram(prog, n_opts, opts.data());
   size_t log_size = 0;
   nvrtcGetProgramLogSize(prog, &log_size);
   std::string plog(log_size, '\0');
@@ -464,7 +615,7 @@ extern "C" {
 int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t* cubin_bytes) {
   if (!fragment) return set_err(nullptr, MUSR_ERR_ARG, "NULL fragment");
   std::string cubin;
-  int rc = jit_compile(nullptr, fragment, log, log_cap, &cubin);
+  int rc = jit_compile(nullptr, 8, 2, 2, fragment, log, log_cap, &cubin);
   if (rc != MUSR_OK) return rc;
   if (cubin_bytes) *cubin_bytes = cubin.size();
   return MUSR_OK;
@@ -473,9 +624,16 @@ int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t*
 int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap) {
   if (!c || !fragment) return set_err(c, MUSR_ERR_ARG, "NULL argument");
   CUDA_TRY(c, cudaSetDevice(c->device));
+  int nu = 0;
+  const char* def = std::strstr(fragment, "#define MUSR_NU ");
+  if (!def || std::sscanf(def + 16, "%d", &nu) != 1 || nu < 1)
+    return set_err(c, MUSR_ERR_ARG, "theory fragment must #define MUSR_NU (>= 1)");
   std::string cubin;
-  int rc = jit_compile(c, fragment, log, log_cap, &cubin);
+  if (c->have_data && c->per_thread_data != c->per_thread)  // layout is tied to the tile size
+    return set_err(c, MUSR_ERR_ARG, "tile size changed after upload");
+  int rc = jit_compile(c, c->per_thread, c->stages, c->min_blocks, fragment, log, log_cap, &cubin);
   if (rc != MUSR_OK) return rc;
+  c->n_uniform = nu;
   free_graphs(c);
   if (c->mod) {
     g_drv.ModuleUnload(c->mod);
@@ -483,8 +641,11 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
   }
   c->have_theory = false;
   CU_TRY(c, g_drv.ModuleLoadData(&c->mod, cubin.data()));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0], c->mod, "musr_chi2"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1], c->mod, "musr_mlh"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][0], c->mod, "musr_chi2_f64"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][1], c->mod, "musr_chi2_c32"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][0], c->mod, "musr_mlh_f64"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][1], c->mod, "musr_mlh_c32"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_utab, c->mod, "musr_uniform_table"));
   c->have_theory = true;
   return build_graphs(c);
 }
@@ -504,6 +665,9 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   free_data(c);
 
+  const int64_t tile_terms = (int64_t)kConsumers * c->per_thread;
+  c->per_thread_data = c->per_thread;
+
   std::vector<MusrHist> hv(n_local);
   std::vector<int> th;
   int64_t tiles = 0;
@@ -517,7 +681,7 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
     if (n0_slot[i] < 0 || n0_slot[i] >= p_capacity || nbkg_slot[i] < 0 ||
         nbkg_slot[i] >= p_capacity)
       return set_err(c, MUSR_ERR_ARG, "N0/Nbkg slot outside p_capacity");
-    const int64_t nt = (n_terms[i] + MUSR_TILE_TERMS - 1) / MUSR_TILE_TERMS;
+    const int64_t nt = (n_terms[i] + tile_terms - 1) / tile_terms;
     MusrHist& H = hv[i];
     std::memset(&H, 0, sizeof(H));
     H.n_terms = n_terms[i];
@@ -539,12 +703,32 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
     if (maps[i] < 0)
       return set_err(c, MUSR_ERR_ARG, "negative map entry");
 
+  // Format: c32 when every in-range count is an integer in [0, kTableMax).
+  double max_count = 0.0;
+  bool compact = n_local > 0;
+  for (int i = 0; compact && i < n_local; ++i) {
+    const double* x = counts[i];
+    for (int64_t k = 0; k < n_terms[i]; ++k) {
+      const double v = x[k];
+      if (!(v >= 0.0 && v < (double)kTableMax && v == (double)(int)v)) { compact = false; break; }
+      if (v > max_count) max_count = v;
+    }
+  }
+  if (const char* f = std::getenv("MUSR_FORMAT")) compact = compact && std::strcmp(f, "f64") != 0;
+  c->fmt = compact ? 1 : 0;
+  c->table_size = 0;
+  if (compact) {
+    int ts = 16;
+    while (ts <= (int)max_count) ts <<= 1;
+    c->table_size = ts;
+  }
+
   c->n_global = n_global;
   c->n_local = n_local;
   c->n_tiles = tiles;
   c->p_capacity = p_capacity;
-  c->have_errors = all_err;
-  const size_t terms = (size_t)tiles * MUSR_TILE_TERMS;
+  c->have_errors = all_err || compact;
+  const size_t terms = (size_t)tiles * tile_terms;
 
   auto dalloc = [&](void** p, size_t bytes) -> int {
     if (bytes == 0) bytes = 8;
@@ -559,8 +743,12 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   int rc;
 #define ALLOC(ptr, bytes) \
   if ((rc = dalloc((void**)&(ptr), (bytes))) != MUSR_OK) return rc
-  ALLOC(c->d, terms * 8);
-  if (all_err) ALLOC(c->e, terms * 8);
+  ALLOC(c->d, terms * (compact ? 4 : 8));
+  if (all_err && !compact) {
+    ALLOC(c->e, terms * 8);
+    ALLOC(c->rcp, terms * 8);
+  }
+  if (compact) ALLOC(c->table, (size_t)c->table_size * 16);
   ALLOC(c->env, terms * 8);
   ALLOC(c->tile_hist, (size_t)tiles * 4);
   ALLOC(c->hist, (size_t)n_local * sizeof(MusrHist));
@@ -582,18 +770,46 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   }
   std::memset(c->h_p, 0, (size_t)p_capacity * 8);
 
-  // zero padding of the streams: padded terms are masked in-kernel, zero keeps
-  // them finite and deterministic
-  CUDA_TRY(c, cudaMemsetAsync(c->d, 0, terms * 8, c->stream));
-  if (all_err) CUDA_TRY(c, cudaMemsetAsync(c->e, 0, terms * 8, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(c->env, 0, terms * 8, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  for (int i = 0; i < n_local; ++i) {
-    const size_t off = (size_t)hv[i].tile_start * MUSR_TILE_TERMS;
-    const size_t bytes = (size_t)n_terms[i] * 8;
-    CUDA_TRY(c, cudaMemcpy(c->d + off, counts[i], bytes, cudaMemcpyHostToDevice));
-    if (all_err) CUDA_TRY(c, cudaMemcpy(c->e + off, errors[i], bytes, cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaMemcpy(c->env + off, envelope[i], bytes, cudaMemcpyHostToDevice));
+  // Streams: dataset segments are copied into a zero-padded natural-order
+  // staging buffer, then laid out per tile for the kernel (musr_layout_stream).
+  {
+    double* stage = nullptr;
+    CUDA_TRY(c, cudaMalloc(&stage, terms * 8 + 8));
+    struct Job { void* dst; const double* const* src; int mode; };
+    const Job jobs[4] = {{c->d, counts, compact ? 1 : 0},
+                         {c->env, envelope, 0},
+                         {c->e, errors, 0},
+                         {c->rcp, errors, 2}};
+    int rc2 = MUSR_OK;
+    for (const Job& job : jobs) {
+      if (!job.dst) continue;
+      cudaError_t ce = cudaMemsetAsync(stage, 0, terms * 8, c->stream);
+      for (int i = 0; ce == cudaSuccess && i < n_local; ++i) {
+        const size_t off = (size_t)hv[i].tile_start * tile_terms;
+        ce = cudaMemcpyAsync(stage + off, job.src[i], (size_t)n_terms[i] * 8,
+                             cudaMemcpyHostToDevice, c->stream);
+      }
+      if (ce == cudaSuccess && terms > 0) {
+        // padding must stay finite for the reciprocal stream (1/0 = inf is fine:
+        // padded terms are masked in-kernel)
+        musr_layout_stream<<<(unsigned)((terms + 255) / 256), 256, 0, c->stream>>>(
+            stage, job.dst, terms, (unsigned)c->per_thread, job.mode);
+        ce = cudaGetLastError();
+      }
+      if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
+      if (ce != cudaSuccess) {
+        rc2 = set_err(c, MUSR_ERR_CUDA, fmt("stream upload: %s", cudaGetErrorString(ce)));
+        break;
+      }
+    }
+    cudaFree(stage);
+    if (rc2 != MUSR_OK) return rc2;
+    if (compact) {
+      musr_build_table<<<(c->table_size + 255) / 256, 256, 0, c->stream>>>(c->table,
+                                                                             c->table_size);
+      CUDA_TRY(c, cudaGetLastError());
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
   }
   if (!th.empty())
     CUDA_TRY(c, cudaMemcpy(c->tile_hist, th.data(), th.size() * 4, cudaMemcpyHostToDevice));
@@ -651,6 +867,17 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
   return MUSR_OK;
 }
 
+int musr_debug_trace(musr_ctx* c, int kind, uint64_t* out, int cap, int* n_ctas) {
+  if (!c || !out || !n_ctas) return set_err(c, MUSR_ERR_ARG, "NULL argument");
+  if (!c->trace) return set_err(c, MUSR_ERR_ARG, "handle not built with MUSR_TRACE=1");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  const int n = std::min<int>(cap / 4, (int)c->grid[kind]);
+  CUDA_TRY(c, cudaMemcpy(out, c->trace, (size_t)n * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  *n_ctas = n;
+  return MUSR_OK;
+}
+
 int musr_tiles(const musr_ctx* c, int64_t* n_tiles) {
   if (!c || !n_tiles) return MUSR_ERR_ARG;
   *n_tiles = c->n_tiles;
@@ -682,7 +909,7 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
     for (int i = 0; i < iters; ++i) {
       if (flush_l2) CUDA_TRY(c, cudaMemsetAsync(c->flush, i & 0xff, c->flush_bytes, c->stream));
       CUDA_TRY(c, cudaEventRecord(e0, c->stream));
-      int rc = launch_kernel(c, kind);
+      int rc = launch_kernels(c, kind, false);
       if (rc != MUSR_OK) return rc;
       CUDA_TRY(c, cudaEventRecord(e1, c->stream));
       CUDA_TRY(c, cudaEventSynchronize(e1));

@@ -9,7 +9,7 @@ struct MusrHist {
   long long first_rel;  // first_bin - t0_bin
   long long first_bin;  // absolute first in-range bin (MLH error report)
   double dt;            // bin width (us)
-  int tile_start;       // first global tile of this histogram
+  int tile_start;       // first tile of this dataset
   int n_tiles;
   int n0_slot;          // index of N0 in P (already wrapped like numpy)
   int nbkg_slot;
@@ -20,9 +20,11 @@ struct MusrHist {
 };
 
 struct MusrArgs {
-  const double* d;            // counts, packed tiles
-  const double* e;            // max(1, sqrt(d)), packed tiles (chi2 only)
+  const void* d;              // counts, packed tiles (fp64, or fp32 in the c32 format)
+  const double* e;            // max(1, sqrt(d)), packed tiles (chi2, f64 format)
+  const double* rcp;          // 1 / e, correctly rounded (chi2, f64 format)
   const double* env;          // exp(-t / tau_mu), packed tiles
+  const double2* table;       // c32 chi2: {max(1, sqrt(k)), 1 / that} for k < table_size
   const int* tile_hist;       // tile -> local histogram
   const MusrHist* hist;       // [n_local]
   const double* P;            // parameter vector
@@ -32,7 +34,12 @@ struct MusrArgs {
   unsigned int* count;        // [n_local] tiles finished (self-resetting)
   unsigned long long* bad;    // [n_local] first non-positive bin (self-resetting)
   double* out;                // [2 * n_global]: sums | (bad bin + 1), 0 = none
-  int n_global;
+  double* utab;               // [n_local][MUSR_NU + 2] uniform values, N0, Nbkg
+  int n_global;               // datasets over all ranks
+  int n_local;                // datasets on this device
+  int n_tiles;                // tiles on this device
+  int table_size;             // entries of `table` (c32 format)
+  unsigned long long* trace;  // MUSR_TRACE builds: per-CTA %globaltimer stamps
 };
 
 #endif  // MUSR_LAYOUT_H

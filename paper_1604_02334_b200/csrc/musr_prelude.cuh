@@ -3,6 +3,8 @@
 #ifndef MUSR_PRELUDE_CUH
 #define MUSR_PRELUDE_CUH
 
+#include "musr_math.cuh"
+
 __device__ __forceinline__ double musr_sq(double x) { return __dmul_rn(x, x); }
 
 // np.power with a bin-uniform exponent (numpy 2.x fast paths, measured).

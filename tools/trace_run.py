@@ -1,0 +1,28 @@
+"""Per-CTA timeline of one objective launch (developer tool, MUSR_TRACE=1)."""
+import ctypes as C, os, sys
+from pathlib import Path
+os.environ["MUSR_TRACE"] = "1"
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+from paper_1604_02334_b200 import workloads as W, musr, objective, _lib
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+w = W.WORKLOADS[name]()
+ds = W.synthesize(w)
+s = objective.session_for(ds, w.expr, musr.TAU_MU_US, len(w.params), objective.DeviceBackend())
+for kind in (0, 1):
+    (musr.chi2 if kind == 0 else musr.mlh)(ds, w.expr, w.params)
+    ms = s.time_evals(kind, 3, 1, True) / 3
+    buf = (C.c_uint64 * (4 * 4096))()
+    n = C.c_int()
+    _lib.check(s._lib.musr_debug_trace(s._handle, kind, buf, len(buf), C.byref(n)), s._handle, "trace")
+    t = np.array(buf[: 4 * n.value], dtype=np.int64).reshape(-1, 4).astype(float)
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1e3
+    rel[t == 0] = np.nan
+    print(f"{name} kind={kind} kernel {1e3*ms:.1f} us, {n.value} CTAs")
+    for label, col in (("start", 0), ("first data", 1), ("stage2 done", 2), ("producer exit", 3)):
+        v = rel[:, col]
+        v = v[~np.isnan(v)]
+        if len(v):
+            print(f"  {label:14s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us  (n={len(v)})")
