@@ -1,0 +1,259 @@
+"""GPU parity tests: libmusr_b200.so against the reference (golden vectors)
+and the CPU oracle, through the drop-in API (musr.chi2 / musr.mlh).
+
+Tolerance (north star): objective values and per-dataset contributions
+within 1e-12 relative.  The kernel reproduces the reference's op order and
+pairwise tree exactly, so observed differences are transcendental ulps
+(~1e-16); exact-value cases are asserted exactly.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_1604_02334_b200 as pkg
+from conftest import build_case, hexf, load_golden, rel
+from oracle import musr_oracle as O
+from paper_1604_02334_b200 import objective, workloads
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+META, ARR = load_golden()
+
+
+@pytest.fixture(autouse=True)
+def _device(gpu_ok):
+    yield
+    objective.clear_cache()
+
+
+def _gpu(kind, dss, expr, p, tau=pkg.TAU_MU_US, backend=None):
+    fn = pkg.chi2 if kind == "chi2" else pkg.mlh
+    total = fn(dss, expr, p, backend, pkg.PhysicsConstants(tau_mu=tau))
+    sess = objective.session_for(dss, expr, tau, len(p), backend or pkg.DeviceBackend())
+    return total, sess.per_dataset()
+
+
+def _oracle(kind, dss, expr, p, tau=pkg.TAU_MU_US):
+    per = []
+    fn = O.chi2 if kind == "chi2" else O.mlh
+    return fn(dss, expr, p, tau, musr_error=pkg.MusrError, eval_error=pkg.EvalError,
+              per_dataset=per), per
+
+
+# -- golden vectors from the reference ---------------------------------------------
+
+@pytest.mark.parametrize("case", META["cases"], ids=[c["name"] for c in META["cases"]])
+def test_golden(case):
+    dss, expr, p, tau = build_case(case, ARR, pkg)
+    for kind, want in case["results"].items():
+        if "error" in want:
+            with pytest.raises(Exception) as exc:
+                _gpu(kind, dss, expr, p, tau)
+            assert type(exc.value).__name__ == want["error"]
+            assert str(exc.value) == want["message"]
+            continue
+        total, per = _gpu(kind, dss, expr, p, tau)
+        if case["name"].startswith("exact"):
+            assert total == hexf(want["value"])
+        assert rel(total, hexf(want["value"])) <= TOL, (kind, total, want["value"])
+        for a, b in zip(per, want["per_dataset"]):
+            assert rel(a, hexf(b)) <= TOL
+
+
+# -- named workloads vs the oracle ----------------------------------------------------
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", dict(nbins=1 << 20)),
+                                     ("C3", dict(n_hist=16, nbins=1 << 20)),
+                                     ("C4", dict(n_hist=8, nbins=1 << 18))])
+def test_workloads_vs_oracle(name, kw):
+    w = workloads.WORKLOADS[name](**kw)
+    dss = workloads.synthesize(w)
+    rng = np.random.default_rng(hash(name) % 1000)
+    for trial in range(2):
+        p = w.params * (1.0 + (0.0 if trial == 0 else 0.03) * rng.standard_normal(len(w.params)))
+        for kind in ("chi2", "mlh"):
+            g, gp = _gpu(kind, dss, w.expr, p)
+            o, op = _oracle(kind, dss, w.expr, p)
+            assert rel(g, o) <= TOL, (name, kind, g, o)
+            assert max(rel(a, b) for a, b in zip(gp, op)) <= TOL
+
+
+def test_ragged_fit_ranges_t0_and_tiny_datasets():
+    rng = np.random.default_rng(4)
+    expr = pkg.parse(workloads.EQ6)
+    dss = []
+    for j, n in enumerate([1, 2, 255, 256, 257, 2047, 2048, 2049, 5000, 70001, 3, 130000]):
+        t0 = int(rng.integers(0, 3)) if n > 10 else 0
+        ds = pkg.MusrDataset(j, rng.poisson(200.0, n), 10.0 / 5000, t0,
+                             pkg.TheoryBinding(map=(0, 1, 2, 3, 0), function_values=(22.5 * j,)), 4, 5)
+        if j % 3 == 1 and n > 10:
+            ds.fit_range = (0.5 * ds.dt * n / 10, 0.9 * ds.dt * n)
+        dss.append(ds)
+    p = np.array([0.25, 0.2, 3.0, 0.05, 200.0, 5.0])
+    for kind in ("chi2", "mlh"):
+        g, gp = _gpu(kind, dss, expr, p)
+        o, op = _oracle(kind, dss, expr, p)
+        assert rel(g, o) <= TOL and max(rel(a, b) for a, b in zip(gp, op)) <= TOL
+
+
+def test_many_datasets_unstaged_path():
+    """> 64 datasets: per-dataset rows are read from global memory."""
+    w = workloads.c4(n_hist=100, nbins=3000)
+    dss = workloads.synthesize(w)
+    for kind in ("chi2", "mlh"):
+        g, gp = _gpu(kind, dss, w.expr, w.params)
+        o, op = _oracle(kind, dss, w.expr, w.params)
+        assert rel(g, o) <= TOL and max(rel(a, b) for a, b in zip(gp, op)) <= TOL
+
+
+def test_non_integer_counts_use_f64_format_and_match():
+    rng = np.random.default_rng(5)
+    expr = pkg.parse("p[m[0]] * se(t, p[m[1]]) * tf(t, p[m[2]], p[m[3]])")
+    dss = [pkg.MusrDataset(0, np.zeros(3), 0.001, 0, pkg.TheoryBinding(map=(0, 1, 2, 3)), 4, 5)]
+    dss[0].counts = rng.uniform(0, 5000, 300000)     # non-integer: f64 streams
+    p = np.array([0.25, 0.5, 30.0, 1.5, 1000.0, 10.0])
+    for kind in ("chi2", "mlh"):
+        assert rel(_gpu(kind, dss, expr, p)[0], _oracle(kind, dss, expr, p)[0]) <= TOL
+
+
+def test_formats_bitwise_identical(monkeypatch):
+    w = workloads.c2(n_hist=3, nbins=100000)
+    dss = workloads.synthesize(w)
+    got = {}
+    for fmt in ("auto", "f64"):
+        monkeypatch.setenv("MUSR_FORMAT", fmt)
+        objective.clear_cache()
+        got[fmt] = [_gpu(k, dss, w.expr, w.params)[0] for k in ("chi2", "mlh")]
+    assert got["auto"] == got["f64"]
+
+
+# -- reference-test ports (test_musr.py, test_acceptance.py) ---------------------------
+
+def _flat(counts, dt=0.01, t0=0, j=0):
+    return pkg.MusrDataset(j, np.asarray(counts), dt, t0, pkg.TheoryBinding(map=()), 0, 1)
+
+
+def test_exact_values():
+    zero = pkg.parse("0 * t")
+    p = np.array([100.0, 5.0])
+    ds = _flat(np.zeros(50))
+    ds.counts = O.model_expected(ds, zero, p)             # numpy model, as test_musr.py:100-104
+    assert pkg.chi2([ds], zero, p) == 0.0
+    assert pkg.chi2([_flat([4])], zero, np.array([0.0, 2.0])) == 1.0
+    assert pkg.mlh([_flat(np.full(100, 7))], zero, np.array([0.0, 7.0])) == 0.0
+    assert pkg.mlh([_flat([0])], zero, np.array([0.0, 3.0])) == 6.0
+    base = np.full(200, 9)
+    assert pkg.mlh([_flat(base)], pkg.parse("0"), np.array([0.0, 9.0])) == 0.0
+    for b in (0, 57, 199):
+        for delta in (-1, 1):
+            c = base.copy()
+            c[b] += delta
+            assert pkg.mlh([_flat(c)], pkg.parse("0"), np.array([0.0, 9.0])) > 0.0
+
+
+def test_mlh_first_nonpositive_bin_in_large_dataset():
+    expr = pkg.parse("p[m[0]] * t")
+    ds = pkg.MusrDataset(3, np.full(500000, 50), 0.001, 11, pkg.TheoryBinding(map=(2,)), 0, 1)
+    # model = (1 * env) * (1 + a*t) + 0 turns non-positive where a*t <= -1
+    p = np.array([1.0, 0.0, -1.0 / 300.0])
+    with pytest.raises(pkg.MusrError) as exc:
+        pkg.mlh([ds], expr, p)
+    with pytest.raises(Exception) as ref_exc:
+        O.mlh([ds], expr, p, musr_error=pkg.MusrError)
+    assert str(exc.value) == str(ref_exc.value)
+
+
+def test_determinism_and_dataset_split():
+    w = workloads.c2(n_hist=4, nbins=200000)
+    dss = workloads.synthesize(w)
+    a = pkg.chi2(dss, w.expr, w.params)
+    assert all(pkg.chi2(dss, w.expr, w.params) == a for _ in range(5))
+    folded = 0.0
+    for ds in dss:
+        folded = folded + pkg.chi2([ds], w.expr, w.params)   # musr.py:190-201
+    assert folded == a
+
+
+def test_collective_path_world1_matches():
+    """The NCCL (sharded) handle with world size 1 gives identical bits."""
+    w = workloads.c2(n_hist=3, nbins=50000)
+    dss = workloads.synthesize(w)
+    plain = [pkg.chi2(dss, w.expr, w.params), pkg.mlh(dss, w.expr, w.params)]
+    be = pkg.DeviceBackend(collective=True, nccl_id=objective.new_nccl_id())
+    coll = [pkg.chi2(dss, w.expr, w.params, be), pkg.mlh(dss, w.expr, w.params, be)]
+    assert plain == coll
+
+
+def test_session_invalidation_on_mutation():
+    w = workloads.c1(nbins=4096)
+    dss = workloads.synthesize(w)
+    a = pkg.chi2(dss, w.expr, w.params)
+    dss[0].fit_range = (1.0, 5.0)
+    b = pkg.chi2(dss, w.expr, w.params)
+    assert b != a and rel(b, O.chi2(dss, w.expr, w.params)) <= TOL
+    dss[0].counts = dss[0].counts + 1.0
+    assert rel(pkg.chi2(dss, w.expr, w.params), O.chi2(dss, w.expr, w.params)) <= TOL
+
+
+# -- fits through the reference minimizer loop -----------------------------------------
+
+def _eq6_problem(n_det, nbins, seed, dt):
+    expr = pkg.parse(workloads.EQ6)
+    truth = np.array([0.25, 0.2, 0.0, 0.05, 1000.0, 10.0])
+    bindings = [pkg.TheoryBinding(map=(0, 1, 2, 3, 0), function_values=(float(ph),))
+                for ph in pkg.default_phases(n_det)]
+    dss = O.generate_synthetic(
+        lambda j, c, d, t0, b, n0, nb: pkg.MusrDataset(j, c, d, t0, b, n0, nb),
+        truth, expr, bindings, [4] * n_det, [5] * n_det, nbins, dt, seed)
+    start = pkg.ParameterSet(values=np.array([0.3, 0.15, 5.0, 0.045, 1000.0, 10.0]),
+                             names=["A0", "sigma", "phi_offset", "B", "N0", "Nbkg"],
+                             step_sizes=np.array([0.01, 0.01, 1.0, 0.001, 1.0, 0.5]),
+                             bounds=[None, (1e-6, np.inf), None, (1e-6, np.inf), None, None],
+                             fixed=np.array([False, False, False, False, True, True]))
+    return dss, expr, start
+
+
+def test_fit_parameters_match_cpu_objective():
+    """Same minimizer loop, GPU objective vs CPU oracle objective: fitted
+    parameters within 1e-9 relative (north-star fit parity)."""
+    dss, expr, start = _eq6_problem(4, 20000, 7, 0.0005)
+    gpu = pkg.minimize("chi2", dss, expr, start)
+    cpu = pkg.minimize("chi2", dss, expr, start, objective_fn=lambda p: O.chi2(dss, expr, p))
+    free = ~start.fixed
+    g, c = gpu.best_parameters.values[free], cpu.best_parameters.values[free]
+    assert np.all(np.abs(g - c) <= 1e-9 * np.abs(c) + 1e-15), (g, c)
+    assert rel(gpu.objective_value, cpu.objective_value) <= TOL
+    assert gpu.objective_value == pkg.chi2(dss, expr, gpu.best_parameters.values)
+
+
+def test_acceptance_criterion_1_fit_recovery():
+    """test_acceptance.py:115-167 on the GPU objective: 16 x 50000 bins."""
+    dss, expr, start = _eq6_problem(16, 50000, 31, 0.0001953125)
+    res = pkg.minimize("chi2", dss, expr, start)
+    best = res.best_parameters
+    ndf = pkg.degrees_of_freedom(dss, best)
+    assert 0.9 <= res.objective_value / ndf <= 1.1
+    slot = best.slot("B")
+
+    def chi2_of_b(b):
+        p = best.values.copy()
+        p[slot] = b
+        return pkg.chi2(dss, expr, p)
+
+    def crossing(direction):
+        step, lo = 1e-5, best.values[slot]
+        while chi2_of_b(lo + direction * step) < res.objective_value + 1.0:
+            step *= 2.0
+        a, c = lo, lo + direction * step
+        for _ in range(60):
+            mid = 0.5 * (a + c)
+            if chi2_of_b(mid) < res.objective_value + 1.0:
+                a = mid
+            else:
+                c = mid
+        return 0.5 * (a + c)
+
+    se = 0.5 * (crossing(+1.0) - crossing(-1.0))
+    assert abs(best.values[slot] - 0.05) <= 3.0 * se

@@ -1,0 +1,240 @@
+"""Host-side logic that needs no GPU: the C ABI surface, the device math
+library compiled for the host, error resolution, sharding, the restated
+Nelder-Mead driver, and the multi-rank result combination (gloo)."""
+
+import ctypes as C
+import os
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1604_02334_b200 as pkg
+from paper_1604_02334_b200 import _lib, objective
+from paper_1604_02334_b200.codegen import lower
+from paper_1604_02334_b200.optimize import MinimizeConfig, nelder_mead
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+# -- C ABI ------------------------------------------------------------------------
+
+def test_library_exports_every_header_symbol():
+    header = (ROOT / "include" / "musr_b200.h").read_text()
+    declared = set(re.findall(r"^\s*(?:int|void|const char\*)\s+(musr_\w+)\s*\(", header, re.M))
+    assert len(declared) >= 14
+    lib = _lib.load()
+    for name in declared:
+        assert hasattr(lib, name), name
+    typed = {name for name, _, _ in _lib.SIGNATURES}
+    assert declared == typed, declared ^ typed
+
+
+def test_library_reports_no_device_cleanly():
+    lib = _lib.load()
+    n = C.c_int(-1)
+    assert lib.musr_device_count(C.byref(n)) == 0
+    if n.value == 0:
+        h = C.c_void_p()
+        assert lib.musr_open(0, C.byref(h)) != 0
+        assert b"device" in lib.musr_global_error().lower()
+
+
+def test_no_cpu_fallback_without_device():
+    """Objective calls raise loudly when no device is present."""
+    if _lib.device_count() > 0:
+        pytest.skip("a device is present")
+    ds = pkg.MusrDataset(0, np.arange(10), 0.1, 0, pkg.TheoryBinding(map=()), 0, 1)
+    with pytest.raises(_lib.MusrDeviceError):
+        pkg.chi2([ds], pkg.parse("0 * t"), np.array([1.0, 2.0]))
+
+
+# -- device math (host build of csrc/musr_math.cuh, IEEE fma from libm) ------------
+
+@pytest.fixture(scope="module")
+def mathlib(tmp_path_factory):
+    out = tmp_path_factory.mktemp("math") / "libmath_host.so"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-Wno-unknown-pragmas",
+                    "-shared", "-fPIC", "-o", str(out),
+                    str(ROOT / "tools" / "mathgen" / "math_host.cpp"), "-lm"], check=True)
+    lib = C.CDLL(str(out))
+
+    def call(name, *arrs):
+        res = np.empty_like(arrs[0])
+        args = [a.ctypes.data_as(C.c_void_p) for a in arrs]
+        getattr(lib, name)(*args, res.ctypes.data_as(C.c_void_p), C.c_long(len(res)))
+        return res
+
+    return call
+
+
+def test_device_exp_within_one_ulp(mathlib):
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.uniform(-708, 708, 400000), rng.uniform(-50, 1, 400000),
+                        [0.0, -0.0, 708.0, -708.0, 709.0, -745.0, np.inf, -np.inf, np.nan]])
+    y = mathlib("v_exp", x)
+    with np.errstate(over="ignore"):
+        ref = np.exp(x)
+    ulps = np.abs(y.view(np.int64) - ref.view(np.int64))
+    finite = np.isfinite(ref) & (ref > 1e-300)
+    assert ulps[finite].max() <= 1
+    assert np.array_equal(np.isnan(y), np.isnan(ref))
+
+
+def test_device_cos_sin_absolute_error(mathlib):
+    rng = np.random.default_rng(1)
+    x = np.concatenate([rng.uniform(-1e4, 1e4, 300000), rng.uniform(-2**20, 2**20, 100000),
+                        np.arange(-500, 500) * np.pi / 2, [0.0, 2.0**20, -2.0**21, 1e300]])
+    for name, f in (("v_cos", np.cos), ("v_sin", np.sin)):
+        y = mathlib(name, x)
+        assert np.abs(y - f(x)).max() <= 4e-16, name
+
+
+def test_markstein_division_is_exact(mathlib):
+    rng = np.random.default_rng(2)
+    n = 1_000_000
+    d = rng.integers(0, 10**6, n).astype(np.float64)
+    e = np.maximum(1.0, np.sqrt(d))
+    y = 1.0 / e
+    for a in (rng.standard_normal(n) * e, d - rng.uniform(0, 2e6, n), np.round(rng.standard_normal(n) * 30),
+              rng.standard_normal(n) * 1e300, rng.uniform(-1e-300, 1e-300, n)):
+        q = mathlib("v_div_y", a, e, y)
+        assert np.array_equal(q.view(np.int64), (a / e).view(np.int64))
+    a = np.array([np.inf, -np.inf, np.nan, 0.0, -0.0])
+    b = np.array([1.0, 3.0, 2.0, 7.0, 7.0])
+    q = mathlib("v_div_y", a, b, 1.0 / b)
+    ref = a / b
+    assert np.array_equal(q[:2], ref[:2]) and np.isnan(q[2])
+    assert np.array_equal(np.signbit(q[3:]), np.signbit(ref[3:]))
+
+
+# -- error resolution ------------------------------------------------------------
+
+def _ds(j, counts, bmap=(), f=(), n0=0, nbkg=1, t0=0, fit=None):
+    ds = pkg.MusrDataset(j, np.asarray(counts), 0.01, t0, pkg.TheoryBinding(map=bmap, function_values=f),
+                         n0, nbkg)
+    ds.fit_range = fit
+    return ds
+
+
+@pytest.mark.parametrize("src,ds,n_p,want", [
+    ("p[m[3]] * t", _ds(0, [5, 6], (0,)), 2, ("EvalError", "slot 3 not covered by map of length 1")),
+    ("p[m[0]] + t", _ds(0, [5, 6], (7,)), 2,
+     ("EvalError", "map entry m[0]=7 out of range for 'p' array of length 2")),
+    ("f[m[1]] + p[m[0]] * t", _ds(0, [5, 6], (0, 2), (0.5,)), 2,
+     ("EvalError", "map entry m[1]=2 out of range for 'f' array of length 1")),
+    ("t + 1 / (2 - 2)", _ds(0, [5, 6]), 2, ("ZeroDivisionError", "float division by zero")),
+    ("0 * t", _ds(0, [5, 6], n0=9), 2, ("IndexError", "index 9 is out of bounds for axis 0 with size 2")),
+    ("0 * t", _ds(0, [5, 6], n0=-2, nbkg=-1), 2, None),
+])
+def test_static_errors(src, ds, n_p, want):
+    err = objective._static_error(ds, lower(pkg.parse(src).ast), n_p, pkg.MusrError, pkg.EvalError)
+    if want is None:
+        assert err is None
+    else:
+        assert (type(err).__name__, str(err)) == want
+
+
+def test_empty_fit_range_detected_at_prepare():
+    low = lower(pkg.parse("0 * t").ast)
+    prep = objective._prepare(1, _ds(1, [1, 2, 3], fit=(100.0, 200.0)), low, 2.197019, 2,
+                              pkg.MusrError, pkg.EvalError, need_streams=False)
+    assert str(prep.error) == "detector 1: empty fit range"
+    prep = objective._prepare(0, _ds(0, np.arange(100), t0=3, fit=(0.1, 0.5)), low, 2.197019, 2,
+                              pkg.MusrError, pkg.EvalError, need_streams=True)
+    t = (np.arange(100) - 3) * 0.01
+    mask = (t >= 0.1) & (t <= 0.5)
+    assert prep.first == np.flatnonzero(mask)[0] and prep.n_terms == mask.sum()
+    assert np.array_equal(prep.envelope, np.exp(-t / 2.197019)[mask])
+    assert np.array_equal(prep.errors, np.maximum(1.0, np.sqrt(np.arange(100.0)))[mask])
+
+
+# -- sharding ------------------------------------------------------------------
+
+def test_shard_assignment_contiguous_balanced():
+    assert objective.shard_assignment([10] * 64, 8) == [r for r in range(8) for _ in range(8)]
+    assert objective.shard_assignment([5, 5], 1) == [0, 0]
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        n = rng.integers(1, 10000, int(rng.integers(1, 70)))
+        world = int(rng.integers(1, 9))
+        owner = objective.shard_assignment(n, world)
+        assert owner == sorted(owner) and max(owner) < world      # contiguous, in range
+        loads = np.bincount(owner, weights=n, minlength=world)
+        assert loads.max() <= n.sum() / world + n.max()
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import musr_oracle as O
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)
+    expr = pkg.parse("p[m[0]] * sg(t, p[m[1]])")
+    dss = [_ds(j, rng.poisson(300, int(rng.integers(500, 3000))), (2, 3)) for j in range(7)]
+    p = np.array([1000.0, 10.0, 0.25, 0.3])
+    owner = objective.shard_assignment([len(d.counts) for d in dss], world)
+    vec = np.zeros(2 * len(dss))                 # sums | bad+1, one contributor per slot
+    for j, ds in enumerate(dss):
+        if owner[j] == rank:
+            vec[j] = O.chi2([ds], expr, p)
+    t = torch.from_numpy(vec)
+    dist.all_reduce(t)                           # stands in for the in-graph ncclAllReduce
+    total = 0.0
+    for s in t.numpy()[: len(dss)]:
+        total = total + s                        # musr.py:190-201 left fold
+    q.put((rank, total, O.chi2(dss, expr, p)))
+    dist.destroy_process_group()
+
+
+def test_sharded_combination_is_exact_gloo():
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, total, single in res:
+        assert total == single   # bitwise: every slot has exactly one non-zero contributor
+
+
+# -- restated Nelder-Mead (optimize.py:41-146) -------------------------------------
+
+def test_minimize_hooks():
+    params = pkg.ParameterSet(values=np.array([0.0]), names=["x"], step_sizes=np.array([0.5]))
+    res = pkg.minimize("chi2", [], pkg.parse("0 * t"), params,
+                       objective_fn=lambda p: (p[0] - 3.0) ** 2)
+    assert res.converged and abs(res.best_parameters.values[0] - 3.0) < 1e-6
+    with pytest.raises(Exception, match="not finite"):
+        pkg.minimize("chi2", [], pkg.parse("0 * t"), params, objective_fn=lambda p: float("nan"))
+    fixed = pkg.ParameterSet(values=np.array([0.0, 5.0]), names=["a", "b"],
+                             step_sizes=np.ones(2), fixed=np.array([True, True]))
+    res = pkg.minimize("chi2", [], pkg.parse("0 * t"), fixed, objective_fn=lambda p: 1.5)
+    assert res.iterations == 0 and res.objective_evaluations == 1 and res.objective_value == 1.5
+
+
+@pytest.mark.ref
+def test_nelder_mead_identical_to_reference(ref):
+    rosen = lambda x: float(sum(100.0 * (x[1:] - x[:-1] ** 2) ** 2 + (1 - x[:-1]) ** 2))
+    bowl = lambda x: float(np.sum((x - np.arange(len(x))) ** 2 * (1 + np.arange(len(x)))))
+    cases = [(rosen, [-1.2, 1.0], [0.1, 0.1], None, None),
+             (rosen, [0.5, 0.5, 0.5, 0.5], [0.2] * 4, [-2] * 4, [0.9] * 4),
+             (bowl, [5.0] * 6, [1.0] * 6, None, None),
+             (bowl, [3.0], [0.5], [1.0], [2.0])]
+    for fn, x0, st, lo, hi in cases:
+        for cfg_args in ({}, {"max_evaluations": 37}, {"restarts": 0, "tol_f": 1e-4}):
+            a = nelder_mead(fn, x0, st, lo, hi, MinimizeConfig(**cfg_args))
+            b = ref.optimize.nelder_mead(fn, x0, st, lo, hi, ref.optimize.MinimizeConfig(**cfg_args))
+            assert np.array_equal(a.x, b.x) and a.fun == b.fun
+            assert (a.iterations, a.evaluations, a.converged) == (b.iterations, b.evaluations, b.converged)
