@@ -114,9 +114,20 @@ int musr_eval(musr_ctx* ctx, int kind, const double* p, int n_p, double* per_dat
 /* Timing helpers (CUDA events on the handle's stream).
  *   mode 0: `iters` back-to-back graph replays (full evaluation incl. H2D p and
  *           D2H results, no host sync in between) -> *ms = total elapsed.
- *   mode 1: `iters` kernel launches, each bracketed by its own events, with an
- *           L2 flush before each when flush_l2 != 0 -> *ms = summed kernel time. */
-int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, double* ms);
+ *   mode 1: `iters` objective-kernel launches, each bracketed by its own
+ *           events -> *ms = *kernel_ms = summed kernel time.
+ *   mode 2: `iters` graph replays, each bracketed by events -> *ms = summed
+ *           evaluation time, *kernel_ms = summed time of the objective kernel
+ *           inside those same replays (event nodes captured in the graph).
+ *   flush_l2 (modes 1, 2): write 512 MiB before each iteration, outside the
+ *   timed interval, so inputs never start L2-resident. */
+int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, double* ms,
+                    double* kernel_ms);
+
+/* Data format chosen at upload: 0 = f64 streams (32 B/bin for chi2),
+ * 1 = c32 (integral counts < 4096: fp32 counts + fp64 envelope, 12 B/bin, with
+ * a {err, 1/err} table of `table_size` entries in shared memory). */
+int musr_format(const musr_ctx* ctx, int* format, int* table_size);
 
 /* Number of tiles (units of 256*R terms) one evaluation processes here. */
 int musr_tiles(const musr_ctx* ctx, int64_t* n_tiles);

@@ -48,8 +48,10 @@ SIGNATURES = [
       _I32P, _I32P, _I32P, C.c_int, _DP, C.c_int, C.c_int]),
     ("musr_eval", C.c_int, [C.c_void_p, C.c_int, _DP, C.c_int, _DP, _I64P, _DP]),
     ("musr_time_evals", C.c_int,
-     [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+     [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+      C.POINTER(C.c_double)]),
     ("musr_tiles", C.c_int, [C.c_void_p, _I64P]),
+    ("musr_format", C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("musr_debug_trace", C.c_int,
      [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]),
     ("musr_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double)]),

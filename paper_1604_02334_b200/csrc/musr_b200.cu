@@ -194,8 +194,9 @@ struct musr_ctx {
   double* h_out = nullptr;  // pinned, 2 * n_global
   int last_np = -1;
 
-  // graphs (one per kind)
+  // graphs (one per kind), with event nodes around the objective kernel
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  cudaEvent_t kev[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
 
   // sharding
   NcclComm comm = nullptr;
@@ -398,10 +399,12 @@ int build_graphs(musr_ctx* c) {
     if (c->n_tiles > 0) {
       lr = g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1, 1,
                               0, (CUstream)c->stream, params, nullptr);
+      cudaEventRecordWithFlags(c->kev[kind][0], c->stream, cudaEventRecordExternal);
       if (lr == CUDA_SUCCESS)
         lr = g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, kThreads, 1, 1,
                                 (unsigned)c->dyn_smem[kind], (CUstream)c->stream, params,
                                 nullptr);
+      cudaEventRecordWithFlags(c->kev[kind][1], c->stream, cudaEventRecordExternal);
     }
     int nr = 0;
     if (c->comm)
@@ -453,9 +456,12 @@ int open_common(int device, musr_ctx** out, musr_ctx** made) {
   if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(4, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_MIN_BLOCKS")) c->min_blocks = std::max(1, std::min(4, std::atoi(v)));
   ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  for (auto& pair : c->kev)
+    for (auto& ev : pair)
+      if (ce == cudaSuccess) ce = cudaEventCreate(&ev);
   if (ce != cudaSuccess) {
     delete c;
-    return set_err(nullptr, MUSR_ERR_CUDA, fmt("stream: %s", cudaGetErrorString(ce)));
+    return set_err(nullptr, MUSR_ERR_CUDA, fmt("stream/events: %s", cudaGetErrorString(ce)));
   }
   *made = c;
   return MUSR_OK;
@@ -527,6 +533,9 @@ void musr_close(musr_ctx* c) {
   if (c->comm) g_nccl.CommDestroy(c->comm);
   if (c->flush) cudaFree(c->flush);
   if (c->trace) cudaFree(c->trace);
+  for (auto& pair : c->kev)
+    for (auto& ev : pair)
+      if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -878,13 +887,21 @@ int musr_debug_trace(musr_ctx* c, int kind, uint64_t* out, int cap, int* n_ctas)
   return MUSR_OK;
 }
 
+int musr_format(const musr_ctx* c, int* format, int* table_size) {
+  if (!c || !format) return MUSR_ERR_ARG;
+  *format = c->fmt;
+  if (table_size) *table_size = c->table_size;
+  return MUSR_OK;
+}
+
 int musr_tiles(const musr_ctx* c, int64_t* n_tiles) {
   if (!c || !n_tiles) return MUSR_ERR_ARG;
   *n_tiles = c->n_tiles;
   return MUSR_OK;
 }
 
-int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, double* ms) {
+int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, double* ms,
+                    double* kernel_ms) {
   if (!c || !ms || iters < 1) return set_err(c, MUSR_ERR_ARG, "bad timing arguments");
   if (kind != 0 && kind != 1) return set_err(c, MUSR_ERR_ARG, "bad kind");
   if (!c->gexec[kind]) return set_err(c, MUSR_ERR_ARG, "objective not ready");
@@ -892,8 +909,25 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
   cudaEvent_t e0, e1;
   CUDA_TRY(c, cudaEventCreate(&e0));
   CUDA_TRY(c, cudaEventCreate(&e1));
-  double total = 0.0;
-  if (mode == 0) {
+  double total = 0.0, ktotal = 0.0;
+  if ((mode == 1 || mode == 2) && flush_l2 && !c->flush) {
+    c->flush_bytes = (size_t)512 << 20;  // > 126 MB L2
+    CUDA_TRY(c, cudaMalloc(&c->flush, c->flush_bytes));
+  }
+  if (mode == 2) {  // graph replays, each bracketed by events, L2 flushed (untimed) before each
+    for (int i = 0; i < iters; ++i) {
+      if (flush_l2) CUDA_TRY(c, cudaMemsetAsync(c->flush, i & 0xff, c->flush_bytes, c->stream));
+      CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+      CUDA_TRY(c, cudaGraphLaunch(c->gexec[kind], c->stream));
+      CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+      CUDA_TRY(c, cudaEventSynchronize(e1));
+      float f = 0.f, fk = 0.f;
+      CUDA_TRY(c, cudaEventElapsedTime(&f, e0, e1));
+      if (c->n_tiles > 0) CUDA_TRY(c, cudaEventElapsedTime(&fk, c->kev[kind][0], c->kev[kind][1]));
+      total += f;
+      ktotal += fk;
+    }
+  } else if (mode == 0) {
     CUDA_TRY(c, cudaEventRecord(e0, c->stream));
     for (int i = 0; i < iters; ++i) CUDA_TRY(c, cudaGraphLaunch(c->gexec[kind], c->stream));
     CUDA_TRY(c, cudaEventRecord(e1, c->stream));
@@ -902,10 +936,6 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
     CUDA_TRY(c, cudaEventElapsedTime(&f, e0, e1));
     total = f;
   } else {
-    if (flush_l2 && !c->flush) {
-      c->flush_bytes = (size_t)512 << 20;  // > 126 MB L2
-      CUDA_TRY(c, cudaMalloc(&c->flush, c->flush_bytes));
-    }
     for (int i = 0; i < iters; ++i) {
       if (flush_l2) CUDA_TRY(c, cudaMemsetAsync(c->flush, i & 0xff, c->flush_bytes, c->stream));
       CUDA_TRY(c, cudaEventRecord(e0, c->stream));
@@ -917,10 +947,12 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
       CUDA_TRY(c, cudaEventElapsedTime(&f, e0, e1));
       total += f;
     }
+    ktotal = total;
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *ms = total;
+  if (kernel_ms) *kernel_ms = ktotal;
   return MUSR_OK;
 }
 

@@ -379,11 +379,20 @@ class Session:
     def per_dataset(self) -> np.ndarray:
         return self._sums.copy()
 
-    def time_evals(self, kind: int, iters: int, mode: int, flush_l2: bool = False) -> float:
-        ms = C.c_double(0.0)
+    def time_evals(self, kind: int, iters: int, mode: int, flush_l2: bool = False):
+        """Device timing (see musr_time_evals): returns ms for modes 0/1 and
+        (eval_ms, kernel_ms) for mode 2."""
+        ms, kms = C.c_double(0.0), C.c_double(0.0)
         _lib.check(self._lib.musr_time_evals(self._handle, kind, iters, mode, int(flush_l2),
-                                             C.byref(ms)), self._handle, "musr_time_evals")
-        return ms.value
+                                             C.byref(ms), C.byref(kms)),
+                   self._handle, "musr_time_evals")
+        return (ms.value, kms.value) if mode == 2 else ms.value
+
+    def data_format(self) -> str:
+        """'c32' (compact: fp32 counts + err/rcp table) or 'f64' (fp64 streams)."""
+        f, ts = C.c_int(0), C.c_int(0)
+        self._lib.musr_format(self._handle, C.byref(f), C.byref(ts))
+        return "c32" if f.value == 1 else "f64"
 
     def n_tiles(self) -> int:
         n = C.c_int64(0)
