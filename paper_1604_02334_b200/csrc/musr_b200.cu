@@ -191,7 +191,9 @@ struct musr_ctx {
   double* out_send = nullptr;
   double* out_recv = nullptr;
   double* h_p = nullptr;    // pinned
-  double* h_out = nullptr;  // pinned, 2 * n_global
+  double* h_out = nullptr;  // pinned + mapped, 2 * n_global
+  double* h_out_dev = nullptr;  // device alias of h_out (direct path writes here)
+  std::vector<double> last_p;   // parameter vector of the last evaluation (timing replays)
   int last_np = -1;
 
   // graphs (one per kind), with event nodes around the objective kernel
@@ -240,6 +242,7 @@ __global__ void musr_build_table(double2* table, int n) {
 namespace {
 
 constexpr int kThreads = 288;          // MUSR_THREADS: 8 consumer warps + 1 producer warp
+constexpr int kMaxStaged = 64;         // MUSR_MAX_STAGED
 constexpr int kConsumers = 256;        // MUSR_CTHREADS
 
 int set_err(musr_ctx* c, int code, const std::string& msg) {
@@ -296,12 +299,19 @@ void free_data(musr_ctx* c) {
   if (c->h_p) cudaFreeHost(c->h_p);
   if (c->h_out) cudaFreeHost(c->h_out);
   c->h_p = c->h_out = nullptr;
+  c->h_out_dev = nullptr;
   c->have_data = false;
   c->last_np = -1;
 }
 
-MusrArgs make_args(const musr_ctx* c) {
+// Direct-launch path: single GPU, per-dataset rows staged per CTA.  One
+// kernel launch per evaluation, parameters inline in the kernel parameters,
+// results written straight to mapped pinned host memory.
+bool direct_mode(const musr_ctx* c) { return c->comm == nullptr && c->n_local <= kMaxStaged; }
+
+MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   MusrArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.d = c->d;
   a.e = c->e;
   a.rcp = c->rcp;
@@ -316,7 +326,7 @@ MusrArgs make_args(const musr_ctx* c) {
   a.partial = c->partial;
   a.count = c->count;
   a.bad = c->bad;
-  a.out = c->out_send;
+  a.out = direct ? c->h_out_dev : c->out_send;
   a.utab = c->utab;
   a.trace = c->trace;
   a.n_tiles = (int)c->n_tiles;
@@ -325,11 +335,18 @@ MusrArgs make_args(const musr_ctx* c) {
   return a;
 }
 
-// The evaluation's kernels: uniform table, then the objective tiles.
-int launch_kernels(musr_ctx* c, int kind, bool with_table) {
+// The evaluation's kernels: [uniform table,] objective tiles.  `a` carries
+// the parameter vector inline when `pinl` is given (direct path).
+int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
+                   const double* pinl = nullptr, int n_p = -1) {
   if (c->n_tiles == 0) return MUSR_OK;  // rank without datasets
-  MusrArgs a = make_args(c);
+  MusrArgs a = make_args(c, direct);
+  if (n_p >= 0) {
+    a.p_inline = 1;
+    if (n_p) std::memcpy(a.pin, pinl, sizeof(double) * (size_t)n_p);
+  }
   void* params[] = {&a};
+  with_table = with_table && c->n_local > kMaxStaged;
   if (with_table)
     CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1,
                                  1, 0, (CUstream)c->stream, params, nullptr));
@@ -338,7 +355,6 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table) {
   return MUSR_OK;
 }
 
-constexpr int kMaxStaged = 64;          // MUSR_MAX_STAGED
 constexpr int kTableMax = 4096;         // c32 format: counts must be integers < this
 
 // Persistent grid and dynamic shared memory per objective kind.
@@ -397,8 +413,9 @@ int build_graphs(musr_ctx* c) {
     void* params[] = {&a};
     CUresult lr = CUDA_SUCCESS;
     if (c->n_tiles > 0) {
-      lr = g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1, 1,
-                              0, (CUstream)c->stream, params, nullptr);
+      if (c->n_local > kMaxStaged)
+        lr = g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1,
+                                1, 0, (CUstream)c->stream, params, nullptr);
       cudaEventRecordWithFlags(c->kev[kind][0], c->stream, cudaEventRecordExternal);
       if (lr == CUDA_SUCCESS)
         lr = g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, kThreads, 1, 1,
@@ -772,8 +789,9 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
 #undef ALLOC
   if (cudaHostAlloc((void**)&c->h_p, (size_t)p_capacity * 8, cudaHostAllocDefault) !=
           cudaSuccess ||
-      cudaHostAlloc((void**)&c->h_out, (size_t)2 * n_global * 8, cudaHostAllocDefault) !=
-          cudaSuccess) {
+      cudaHostAlloc((void**)&c->h_out, (size_t)2 * n_global * 8, cudaHostAllocMapped) !=
+          cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->h_out_dev, c->h_out, 0) != cudaSuccess) {
     free_data(c);
     return set_err(c, MUSR_ERR_NOMEM, "pinned host allocation failed");
   }
@@ -840,6 +858,31 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   return build_graphs(c);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Device work of one evaluation on the handle's stream (no host sync).
+//   direct path: [H2D p if it does not fit inline] + one objective launch
+//   graph path : one graph replay (H2D p, [uniform table], objective,
+//                [ncclAllReduce], D2H results)
+int launch_eval(musr_ctx* c, int kind) {
+  if (direct_mode(c)) {
+    const int n_p = (int)c->last_p.size();
+    const bool inline_p = n_p <= MUSR_P_INLINE;
+    if (!inline_p)
+      CUDA_TRY(c, cudaMemcpyAsync(c->P, c->h_p, sizeof(double) * c->p_capacity,
+                                  cudaMemcpyHostToDevice, c->stream));
+    return launch_kernels(c, kind, false, true, c->last_p.data(), inline_p ? n_p : -1);
+  }
+  CUDA_TRY(c, cudaGraphLaunch(c->gexec[kind], c->stream));
+  return MUSR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_dataset,
               int64_t* first_bad_bin, double* total) {
   if (!c) return set_err(c, MUSR_ERR_ARG, "NULL handle");
@@ -854,12 +897,17 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
                                         c->p_capacity));
   if (n_p && !p) return set_err(c, MUSR_ERR_ARG, "p is NULL");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  if (n_p) std::memcpy(c->h_p, p, (size_t)n_p * 8);
-  if (n_p != c->last_np) {
-    if (n_p < c->p_capacity) std::memset(c->h_p + n_p, 0, (size_t)(c->p_capacity - n_p) * 8);
-    c->last_np = n_p;
+  const bool inline_p = n_p <= MUSR_P_INLINE;
+  if (!inline_p || !direct_mode(c)) {
+    if (n_p) std::memcpy(c->h_p, p, (size_t)n_p * 8);
+    if (n_p != c->last_np) {
+      if (n_p < c->p_capacity) std::memset(c->h_p + n_p, 0, (size_t)(c->p_capacity - n_p) * 8);
+      c->last_np = n_p;
+    }
   }
-  CUDA_TRY(c, cudaGraphLaunch(c->gexec[kind], c->stream));
+  c->last_p.assign(p, p + n_p);
+  int rc = launch_eval(c, kind);
+  if (rc != MUSR_OK) return rc;
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   const int G = c->n_global;
   double acc = 0.0;
@@ -914,22 +962,30 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
     c->flush_bytes = (size_t)512 << 20;  // > 126 MB L2
     CUDA_TRY(c, cudaMalloc(&c->flush, c->flush_bytes));
   }
-  if (mode == 2) {  // graph replays, each bracketed by events, L2 flushed (untimed) before each
+  const bool direct = direct_mode(c);
+  if (mode == 2) {  // evaluations, each bracketed by events, L2 flushed (untimed) before each
     for (int i = 0; i < iters; ++i) {
       if (flush_l2) CUDA_TRY(c, cudaMemsetAsync(c->flush, i & 0xff, c->flush_bytes, c->stream));
       CUDA_TRY(c, cudaEventRecord(e0, c->stream));
-      CUDA_TRY(c, cudaGraphLaunch(c->gexec[kind], c->stream));
+      int rc = launch_eval(c, kind);
+      if (rc != MUSR_OK) return rc;
       CUDA_TRY(c, cudaEventRecord(e1, c->stream));
       CUDA_TRY(c, cudaEventSynchronize(e1));
       float f = 0.f, fk = 0.f;
       CUDA_TRY(c, cudaEventElapsedTime(&f, e0, e1));
-      if (c->n_tiles > 0) CUDA_TRY(c, cudaEventElapsedTime(&fk, c->kev[kind][0], c->kev[kind][1]));
+      if (direct)
+        fk = f;  // the evaluation is the objective kernel
+      else if (c->n_tiles > 0)
+        CUDA_TRY(c, cudaEventElapsedTime(&fk, c->kev[kind][0], c->kev[kind][1]));
       total += f;
       ktotal += fk;
     }
   } else if (mode == 0) {
     CUDA_TRY(c, cudaEventRecord(e0, c->stream));
-    for (int i = 0; i < iters; ++i) CUDA_TRY(c, cudaGraphLaunch(c->gexec[kind], c->stream));
+    for (int i = 0; i < iters; ++i) {
+      int rc = launch_eval(c, kind);
+      if (rc != MUSR_OK) return rc;
+    }
     CUDA_TRY(c, cudaEventRecord(e1, c->stream));
     CUDA_TRY(c, cudaEventSynchronize(e1));
     float f = 0.f;
@@ -939,7 +995,7 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
     for (int i = 0; i < iters; ++i) {
       if (flush_l2) CUDA_TRY(c, cudaMemsetAsync(c->flush, i & 0xff, c->flush_bytes, c->stream));
       CUDA_TRY(c, cudaEventRecord(e0, c->stream));
-      int rc = launch_kernels(c, kind, false);
+      int rc = direct ? launch_eval(c, kind) : launch_kernels(c, kind, false);
       if (rc != MUSR_OK) return rc;
       CUDA_TRY(c, cudaEventRecord(e1, c->stream));
       CUDA_TRY(c, cudaEventSynchronize(e1));

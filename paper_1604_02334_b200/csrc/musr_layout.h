@@ -4,6 +4,10 @@
 #ifndef MUSR_LAYOUT_H
 #define MUSR_LAYOUT_H
 
+// Parameter vectors up to this length travel inside the kernel parameters
+// (no H2D copy per evaluation); longer ones use the device buffer `P`.
+#define MUSR_P_INLINE 128
+
 struct MusrHist {
   long long n_terms;    // in-range bins
   long long first_rel;  // first_bin - t0_bin
@@ -40,6 +44,9 @@ struct MusrArgs {
   int n_tiles;                // tiles on this device
   int table_size;             // entries of `table` (c32 format)
   unsigned long long* trace;  // MUSR_TRACE builds: per-CTA %globaltimer stamps
+  int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
+  int pad_;
+  double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)
 };
 
 #endif  // MUSR_LAYOUT_H
