@@ -157,12 +157,14 @@ struct musr_ctx {
   bool have_theory = false;
   int n_uniform = 1;            // MUSR_NU of the loaded theory
   int sms = 0;                  // multiprocessors on the device
-  int per_thread = 8;           // MUSR_PT: terms per consumer thread; tile = 256 * per_thread
+  int per_thread = 8;           // MUSR_PT: terms per consumer thread
+  int cwarps = 16;              // MUSR_CWARPS: consumer warps per CTA; tile = 32*cwarps*per_thread
   int stages = 2;               // MUSR_STAGES: TMA pipeline depth
-  int min_blocks = 2;           // MUSR_MIN_BLOCKS: register budget target
+  int min_blocks = 1;           // MUSR_MIN_BLOCKS: register budget target
   double* utab = nullptr;       // uniform table (sized at graph build)
   size_t utab_rows = 0;
   unsigned long long* trace = nullptr;  // MUSR_TRACE=1: per-CTA timeline
+  unsigned* sched = nullptr;    // [2] dynamic tile scheduler (self-resetting)
   unsigned grid[2] = {0, 0};    // persistent grid per kind
   size_t dyn_smem[2] = {0, 0};  // dynamic shared memory per kind
   int per_thread_data = 8;      // per_thread the uploaded layout was padded for
@@ -208,20 +210,20 @@ struct musr_ctx {
   size_t flush_bytes = 0;
 };
 
-// Tile layout of one stream (musr_kernel.cuh): tiles of 256*pt terms; inside a
-// tile the 16-byte group k*256 + t holds thread t's elements g*k .. g*k+g-1
+// Tile layout of one stream (musr_kernel.cuh): tiles of cthreads*pt terms; inside
+// a tile the 16-byte group k*cthreads + t holds thread t's elements g*k .. g*k+g-1
 // (g = 16 / element size), so consumer reads are conflict-free LDS.128.
 // mode 0: fp64 copy, 1: fp32 (exact for the c32 format), 2: fp64 reciprocal
 // (__drcp_rn == IEEE 1.0/x, the Markstein divisor of musr_div_y).
 __global__ void musr_layout_stream(const double* __restrict__ src, void* __restrict__ dst,
-                                   size_t terms, unsigned pt, int mode) {
+                                   size_t terms, unsigned pt, unsigned cthreads, int mode) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= terms) return;
-  const size_t tile_terms = 256u * pt;
+  const size_t tile_terms = (size_t)cthreads * pt;
   const size_t tile = i / tile_terms;
   const unsigned r = (unsigned)(i - tile * tile_terms);
   const unsigned g = (mode == 1) ? 4u : 2u;
-  const unsigned grp = r / g, e = r - grp * g, k = grp >> 8, t = grp & 255u;
+  const unsigned grp = r / g, e = r - grp * g, k = grp / cthreads, t = grp % cthreads;
   const double v = src[tile * tile_terms + (size_t)t * pt + g * k + e];
   if (mode == 1)
     static_cast<float*>(dst)[i] = (float)v;
@@ -241,9 +243,7 @@ __global__ void musr_build_table(double2* table, int n) {
 
 namespace {
 
-constexpr int kThreads = 288;          // MUSR_THREADS: 8 consumer warps + 1 producer warp
 constexpr int kMaxStaged = 64;         // MUSR_MAX_STAGED
-constexpr int kConsumers = 256;        // MUSR_CTHREADS
 
 int set_err(musr_ctx* c, int code, const std::string& msg) {
   if (c) c->err = msg; else g_error = msg;
@@ -278,7 +278,8 @@ void free_graphs(musr_ctx* c) {
 void free_data(musr_ctx* c) {
   free_graphs(c);
   void* dev[] = {c->d, c->e, c->rcp, c->env, c->table, c->tile_hist, c->hist, c->P, c->maps,
-                 c->fvals, c->partial, c->count, c->bad, c->out_send, c->out_recv, c->utab};
+                 c->fvals, c->partial, c->count, c->bad, c->out_send, c->out_recv, c->utab,
+                 c->sched};
   for (void* p : dev)
     if (p) cudaFree(p);
   c->d = nullptr;
@@ -296,6 +297,7 @@ void free_data(musr_ctx* c) {
   c->out_send = c->out_recv = nullptr;
   c->utab = nullptr;
   c->utab_rows = 0;
+  c->sched = nullptr;
   if (c->h_p) cudaFreeHost(c->h_p);
   if (c->h_out) cudaFreeHost(c->h_out);
   c->h_p = c->h_out = nullptr;
@@ -329,6 +331,7 @@ MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   a.out = direct ? c->h_out_dev : c->out_send;
   a.utab = c->utab;
   a.trace = c->trace;
+  a.sched = c->sched;
   a.n_tiles = (int)c->n_tiles;
   a.n_global = c->n_global;
   a.n_local = c->n_local;
@@ -350,7 +353,7 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
   if (with_table)
     CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1,
                                  1, 0, (CUstream)c->stream, params, nullptr));
-  CU_TRY(c, g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, kThreads, 1, 1,
+  CU_TRY(c, g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, 32 * (c->cwarps + 1), 1, 1,
                                (unsigned)c->dyn_smem[kind], (CUstream)c->stream, params, nullptr));
   return MUSR_OK;
 }
@@ -359,12 +362,13 @@ constexpr int kTableMax = 4096;         // c32 format: counts must be integers <
 
 // Persistent grid and dynamic shared memory per objective kind.
 int plan_launch(musr_ctx* c) {
-  const size_t tile = (size_t)kConsumers * c->per_thread;  // terms per tile
+  const size_t tile = (size_t)32 * c->cwarps * c->per_thread;  // terms per tile
   for (int kind = 0; kind < 2; ++kind) {
     // MusrGeom in musr_kernel.cuh: d | env | err | rcp
     size_t stage = tile * (c->fmt ? 4 : 8) + tile * 8;
     if (kind == 0 && c->fmt == 0) stage += 2 * tile * 8;
-    size_t smem = (size_t)c->stages * stage;
+    const int stages = (kind == 0 && c->fmt == 0 && tile * 32 > 96 * 1024) ? 1 : c->stages;
+    size_t smem = (size_t)stages * stage;  // mirrors the stage count in musr_kernel.cuh
     if (kind == 0 && c->fmt == 1) smem += (size_t)c->table_size * 16;
     if (c->n_local <= kMaxStaged)
       smem += (size_t)c->n_local * (c->n_uniform + 2) * sizeof(double);
@@ -373,7 +377,8 @@ int plan_launch(musr_ctx* c) {
     CU_TRY(c, g_drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                                      (int)smem));
     int occ = 0;
-    CU_TRY(c, g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
+    CU_TRY(c, g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * (c->cwarps + 1),
+                                                               smem));
     if (occ < 1) return set_err(c, MUSR_ERR_CUDA, "objective kernel does not fit on an SM");
     const int64_t cap = (int64_t)c->sms * occ;
     c->grid[kind] = (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, cap));
@@ -418,7 +423,7 @@ int build_graphs(musr_ctx* c) {
                                 1, 0, (CUstream)c->stream, params, nullptr);
       cudaEventRecordWithFlags(c->kev[kind][0], c->stream, cudaEventRecordExternal);
       if (lr == CUDA_SUCCESS)
-        lr = g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, kThreads, 1, 1,
+        lr = g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, 32 * (c->cwarps + 1), 1, 1,
                                 (unsigned)c->dyn_smem[kind], (CUstream)c->stream, params,
                                 nullptr);
       cudaEventRecordWithFlags(c->kev[kind][1], c->stream, cudaEventRecordExternal);
@@ -472,6 +477,8 @@ int open_common(int device, musr_ctx** out, musr_ctx** made) {
   if (const char* v = std::getenv("MUSR_PT")) c->per_thread = std::atoi(v) == 4 ? 4 : 8;
   if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(4, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_MIN_BLOCKS")) c->min_blocks = std::max(1, std::min(4, std::atoi(v)));
+  if (const char* v = std::getenv("MUSR_CWARPS")) c->cwarps = std::atoi(v) == 8 ? 8 : 16;
+  if (c->cwarps == 16) c->min_blocks = std::min(c->min_blocks, 1);  // 544 threads: one CTA per SM
   ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   for (auto& pair : c->kev)
     for (auto& ev : pair)
@@ -564,7 +571,8 @@ const char* musr_last_error(const musr_ctx* c) { return c ? c->err.c_str() : g_e
 namespace {
 
 // NVRTC: (prelude + fragment + kernel template) -> sm_100a CUBIN, cached by source.
-int jit_compile(musr_ctx* c, int per_thread, int stages, int min_blocks, const char* fragment,
+int jit_compile(musr_ctx* c, int per_thread, int stages, int min_blocks, int cwarps,
+                const char* fragment,
                 char* log, size_t log_cap, std::string* cubin) {
   std::string src = std::string("#include \"musr_prelude.cuh\"\n// generated theory\n") + fragment +
                     "\n#include \"musr_kernel.cuh\"\n";
@@ -572,7 +580,8 @@ int jit_compile(musr_ctx* c, int per_thread, int stages, int min_blocks, const c
                                     "-lineinfo", "--prec-div=true", "--prec-sqrt=true",
                                     "--ftz=false", "-DMUSR_PT=" + std::to_string(per_thread),
                                     "-DMUSR_STAGES=" + std::to_string(stages),
-                                    "-DMUSR_MIN_BLOCKS=" + std::to_string(min_blocks)};
+                                    "-DMUSR_MIN_BLOCKS=" + std::to_string(min_blocks),
+                                    "-DMUSR_CWARPS=" + std::to_string(cwarps)};
   if (std::getenv("MUSR_TRACE")) opt_s.push_back("-DMUSR_TRACE");
   // tuning hook: extra NVRTC options (e.g. "-DMUSR_PREFETCH=0 -DMUSR_MIN_BLOCKS=3")
   if (const char* extra = std::getenv("MUSR_NVRTC_OPTS")) {
@@ -641,7 +650,7 @@ extern "C" {
 int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t* cubin_bytes) {
   if (!fragment) return set_err(nullptr, MUSR_ERR_ARG, "NULL fragment");
   std::string cubin;
-  int rc = jit_compile(nullptr, 8, 2, 2, fragment, log, log_cap, &cubin);
+  int rc = jit_compile(nullptr, 8, 2, 1, 16, fragment, log, log_cap, &cubin);
   if (rc != MUSR_OK) return rc;
   if (cubin_bytes) *cubin_bytes = cubin.size();
   return MUSR_OK;
@@ -655,9 +664,10 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
   if (!def || std::sscanf(def + 16, "%d", &nu) != 1 || nu < 1)
     return set_err(c, MUSR_ERR_ARG, "theory fragment must #define MUSR_NU (>= 1)");
   std::string cubin;
-  if (c->have_data && c->per_thread_data != c->per_thread)  // layout is tied to the tile size
+  if (c->have_data && c->per_thread_data != c->per_thread * 100 + c->cwarps)  // layout <-> tile
     return set_err(c, MUSR_ERR_ARG, "tile size changed after upload");
-  int rc = jit_compile(c, c->per_thread, c->stages, c->min_blocks, fragment, log, log_cap, &cubin);
+  int rc = jit_compile(c, c->per_thread, c->stages, c->min_blocks, c->cwarps, fragment, log,
+                       log_cap, &cubin);
   if (rc != MUSR_OK) return rc;
   c->n_uniform = nu;
   free_graphs(c);
@@ -691,8 +701,8 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   free_data(c);
 
-  const int64_t tile_terms = (int64_t)kConsumers * c->per_thread;
-  c->per_thread_data = c->per_thread;
+  const int64_t tile_terms = (int64_t)32 * c->cwarps * c->per_thread;
+  c->per_thread_data = c->per_thread * 100 + c->cwarps;
 
   std::vector<MusrHist> hv(n_local);
   std::vector<int> th;
@@ -783,6 +793,7 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   ALLOC(c->fvals, (size_t)n_local * f_stride * 8);
   ALLOC(c->partial, (size_t)tiles * 8);
   ALLOC(c->count, (size_t)n_local * 4);
+  ALLOC(c->sched, 2 * sizeof(unsigned));
   ALLOC(c->bad, (size_t)n_local * 8);
   ALLOC(c->out_send, (size_t)2 * n_global * 8);
   ALLOC(c->out_recv, (size_t)2 * n_global * 8);
@@ -820,7 +831,7 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
         // padding must stay finite for the reciprocal stream (1/0 = inf is fine:
         // padded terms are masked in-kernel)
         musr_layout_stream<<<(unsigned)((terms + 255) / 256), 256, 0, c->stream>>>(
-            stage, job.dst, terms, (unsigned)c->per_thread, job.mode);
+            stage, job.dst, terms, (unsigned)c->per_thread, (unsigned)(32 * c->cwarps), job.mode);
         ce = cudaGetLastError();
       }
       if (ce == cudaSuccess) ce = cudaStreamSynchronize(c->stream);
@@ -851,6 +862,7 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
                            cudaMemcpyHostToDevice));
   }
   CUDA_TRY(c, cudaMemset(c->count, 0, (size_t)n_local * 4));
+  CUDA_TRY(c, cudaMemset(c->sched, 0, 2 * sizeof(unsigned)));
   CUDA_TRY(c, cudaMemset(c->bad, 0xff, (size_t)n_local * 8));
   CUDA_TRY(c, cudaMemset(c->out_send, 0, (size_t)2 * n_global * 8));
   CUDA_TRY(c, cudaMemset(c->out_recv, 0, (size_t)2 * n_global * 8));

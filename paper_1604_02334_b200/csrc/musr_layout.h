@@ -44,6 +44,7 @@ struct MusrArgs {
   int n_tiles;                // tiles on this device
   int table_size;             // entries of `table` (c32 format)
   unsigned long long* trace;  // MUSR_TRACE builds: per-CTA %globaltimer stamps
+  unsigned int* sched;        // [2] dynamic tile scheduler: next tile, exited CTAs (self-resetting)
   int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
   int pad_;
   double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)

@@ -21,7 +21,13 @@ for kind in (0, 1):
     rel = (t - t0) / 1e3
     rel[t == 0] = np.nan
     print(f"{name} kind={kind} kernel {1e3*ms:.1f} us, {n.value} CTAs")
-    for label, col in (("start", 0), ("first data", 1), ("stage2 done", 2), ("producer exit", 3)):
+    tiles = np.array(buf[: 4 * n.value], dtype=np.int64).reshape(-1, 4)[:, 2]
+    ex = rel[:, 3]
+    order = np.argsort(ex)
+    print("  tiles/CTA min %d max %d; 10 latest CTAs (exit us, tiles): %s" % (
+        tiles.min(), tiles.max(), [(round(ex[i], 1), int(tiles[i])) for i in order[-10:]]))
+    print("  10 earliest: %s" % [(round(ex[i], 1), int(tiles[i])) for i in order[:10]])
+    for label, col in (("start", 0), ("first data", 1), ("producer exit", 3)):
         v = rel[:, col]
         v = v[~np.isnan(v)]
         if len(v):
