@@ -282,6 +282,108 @@ class _Emitter:
         return f"pow({base}, {self.value(ex)})"
 
 
+class _VecEmitter:
+    """Per-bin body vectorised over a thread's MUSR_PT consecutive bins.
+
+    Per-bin values are arrays ``vN[MUSR_PT]``; bin-uniform ones are scalars.
+    exp and bin-uniform-exponent pow are *anchored* on the run's first bin
+    (csrc/musr_math.cuh: musr_exp_anchored / musr_pow_anchored): one full
+    evaluation per run plus a short series per further bin, with the error
+    bounded per bin (no accumulation).  cos/sin use the fast per-bin form.
+    Any argument outside a fast form's window clears ``ok``.
+    """
+
+    def __init__(self, scalar_leaf, uniform_of):
+        self.lines: List[str] = []
+        self.names: Dict[Node, str] = {}
+        self.scalar_leaf = scalar_leaf   # uniform node -> C expression (U[k] / literal)
+        self.uniform_of = uniform_of
+        self.n = 0
+
+    def _fresh(self) -> str:
+        self.n += 1
+        return f"w{self.n}"
+
+    def ref(self, node: Node, j: str) -> str:
+        """C expression of `node` at bin index expression `j`."""
+        if isinstance(node, Num):
+            return _lit(float(node.value))
+        if isinstance(node, TimeVar):
+            return f"t[{j}]"
+        if self.uniform_of(node):
+            return self.scalar_leaf(node)
+        return f"{self.vec(node)}[{j}]"
+
+    def _loop(self, name: str, body: str, first: int = 0) -> None:
+        self.lines.append(f"  #pragma unroll")
+        self.lines.append(f"  for (int j = {first}; j < MUSR_PT; ++j) {name}[j] = {body};")
+
+    def vec(self, node: Node) -> str:
+        if node in self.names:
+            return self.names[node]
+        name = self._fresh()
+        self.lines.append(f"  double {name}[MUSR_PT];")
+        if isinstance(node, Unary):
+            self._loop(name, f"(-{self.ref(node.operand, 'j')})")
+        elif isinstance(node, Binary) and node.op != "^":
+            self._loop(name, f"{_ARITH[node.op]}({self.ref(node.left, 'j')}, {self.ref(node.right, 'j')})")
+        elif isinstance(node, Binary):
+            self._pow(name, node)
+        elif isinstance(node, Call):
+            self._call(name, node)
+        else:
+            raise TheoryError(f"cannot vectorise {node!r}")
+        self.names[node] = name
+        return name
+
+    def _call(self, name: str, node: Call) -> None:
+        arg = node.args[0]
+        if node.name == "exp":
+            x = self.vec(arg) if not self.uniform_of(arg) else None
+            if x is None:  # cannot happen: uniform calls are hoisted
+                raise TheoryError("uniform exp reached the vector emitter")
+            self.lines.append(f"  {name}[0] = musr_exp_fast({x}[0], ok);")
+            self._loop(name, f"musr_exp_anchored({x}[j], {x}[0], {name}[0], ok)", first=1)
+        elif node.name in ("cos", "sin"):
+            self._loop(name, f"musr_{node.name}_fast({self.ref(arg, 'j')}, ok)")
+        elif node.name == "sqrt":
+            self._loop(name, f"__dsqrt_rn({self.ref(arg, 'j')})")
+        else:
+            self._loop(name, f"{_FUNC_EXACT[node.name]}({self.ref(arg, 'j')})")
+
+    def _pow(self, name: str, node: Binary) -> None:
+        base, ex = node.left, node.right
+        if not self.uniform_of(base) and not isinstance(base, TimeVar):
+            self.vec(base)  # materialise before any branch so every path can use it
+        bj = lambda: self.ref(base, "j")
+        if isinstance(ex, Num):
+            e = float(ex.value)
+            special = {2.0: "musr_sq({b})", 0.5: "__dsqrt_rn({b})", -1.0: "__ddiv_rn(1.0, {b})",
+                       1.0: "{b}", 0.0: "1.0"}
+            if e in special:
+                self._loop(name, special[e].format(b=bj()))
+                return
+            self._anchored_pow(name, base, _lit(e))
+            return
+        if self.uniform_of(ex):
+            b = self.scalar_leaf(ex)
+            self.lines.append(f"  if ({b} == 2.0 || {b} == 0.5 || {b} == -1.0 || {b} == 1.0 || {b} == 0.0) {{")
+            self._loop(name, f"musr_npy_pow_u({bj()}, {b})")
+            self.lines.append("  } else {")
+            self._anchored_pow(name, base, b)
+            self.lines.append("  }")
+            return
+        self._loop(name, f"pow({bj()}, {self.ref(ex, 'j')})")
+
+    def _anchored_pow(self, name: str, base: Node, b: str) -> None:
+        x0 = self.ref(base, "0")
+        self.lines.append(f"  {{ const double p0_ = pow({x0}, {b});")
+        self.lines.append(f"    const MusrPowAnchor an_ = musr_pow_anchor({x0}, p0_, {b});")
+        self.lines.append(f"    {name}[0] = p0_;")
+        self.lines.append(f"    #pragma unroll")
+        self.lines.append(f"    for (int j = 1; j < MUSR_PT; ++j) {name}[j] = musr_pow_anchored({self.ref(base, 'j')}, an_, ok); }}")
+
+
 def lower(ast: Node) -> Lowered:
     events: List[StaticEvent] = []
     folded, pyval = _events_and_fold(ast, events)
@@ -370,6 +472,26 @@ def lower(ast: Node) -> Lowered:
     src.append("  (void)t; (void)U; (void)ok;")
     src.extend(bodies[True][0])
     src.append(f"  return {bodies[True][1]};")
+    src.append("}")
+    # vectorised per-thread body (anchored transcendentals)
+    ve = _VecEmitter(lambda n: _lit(float(n.value)) if isinstance(n, Num) else f"U[{hoisted[n]}]",
+                     uniform)
+    if per_bin:
+        vres = ve.vec(prim) if not isinstance(prim, TimeVar) else None
+    src.append("__device__ __forceinline__ void musr_theory_vec(const double (&t)[MUSR_PT], "
+               "const double* __restrict__ U, double (&A)[MUSR_PT], bool& ok) {")
+    src.append("  (void)t; (void)U; (void)ok;")
+    if not per_bin:
+        val = _lit(float(prim.value)) if isinstance(prim, Num) else f"U[{hoisted[prim]}]"
+        src.append("  #pragma unroll")
+        src.append(f"  for (int j = 0; j < MUSR_PT; ++j) A[j] = {val};")
+    elif isinstance(prim, TimeVar):
+        src.append("  #pragma unroll")
+        src.append("  for (int j = 0; j < MUSR_PT; ++j) A[j] = t[j];")
+    else:
+        src.extend(ve.lines)
+        src.append("  #pragma unroll")
+        src.append(f"  for (int j = 0; j < MUSR_PT; ++j) A[j] = {vres}[j];")
     src.append("}")
     src.append("__device__ __noinline__ double musr_theory_exact(const double t, "
                "const double* __restrict__ U) {")

@@ -6,7 +6,13 @@
 
 // Parameter vectors up to this length travel inside the kernel parameters
 // (no H2D copy per evaluation); longer ones use the device buffer `P`.
-#define MUSR_P_INLINE 128
+#define MUSR_P_INLINE 64
+// Small problems (<= MUSR_H_INLINE datasets, short map / f rows) also carry
+// their per-dataset metadata, maps and function values inline, so the CTA
+// prologue reads only kernel-parameter space (no dependent global loads).
+#define MUSR_H_INLINE 16
+#define MUSR_M_INLINE 12
+#define MUSR_F_INLINE 4
 
 struct MusrHist {
   long long n_terms;    // in-range bins
@@ -46,8 +52,11 @@ struct MusrArgs {
   unsigned long long* trace;  // MUSR_TRACE builds: per-CTA %globaltimer stamps
   unsigned int* sched;        // [2] dynamic tile scheduler: next tile, exited CTAs (self-resetting)
   int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
-  int pad_;
+  int h_inline;               // 1: hin/min/fin hold all datasets' metadata
   double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)
+  MusrHist hin[MUSR_H_INLINE];
+  int min[MUSR_H_INLINE][MUSR_M_INLINE];
+  double fin[MUSR_H_INLINE][MUSR_F_INLINE];
 };
 
 #endif  // MUSR_LAYOUT_H

@@ -5,6 +5,10 @@
 
 #include "musr_math.cuh"
 
+#ifndef MUSR_PT
+#define MUSR_PT 8  // bins per consumer thread (musr_theory_vec works on one run)
+#endif
+
 __device__ __forceinline__ double musr_sq(double x) { return __dmul_rn(x, x); }
 
 // np.power with a bin-uniform exponent (numpy 2.x fast paths, measured).

@@ -8,6 +8,22 @@ extern "C" {
 void v_exp(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = musr_exp(x[i]); }
 void v_cos(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = musr_cos(x[i]); }
 void v_sin(const double* x, double* y, long n) { for (long i = 0; i < n; ++i) y[i] = musr_sin(x[i]); }
+void v_exp_anchored(const double* x, const double* x0, double* y, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    const double e0 = musr_exp(x0[i]);
+    y[i] = musr_exp_anchored(x[i], x0[i], e0, ok);
+    if (!ok) y[i] = NAN;
+  }
+}
+void v_pow_anchored(const double* x, const double* x0, const double* b, double* y, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    const MusrPowAnchor a = musr_pow_anchor(x0[i], pow(x0[i], b[i]), b[i]);
+    y[i] = musr_pow_anchored(x[i], a, ok);
+    if (!ok) y[i] = NAN;
+  }
+}
 void v_div_y(const double* a, const double* b, const double* yb, double* q, long n) {
   for (long i = 0; i < n; ++i) q[i] = musr_div_y(a[i], b[i], yb[i]);
 }

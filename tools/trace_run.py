@@ -27,7 +27,7 @@ for kind in (0, 1):
     print("  tiles/CTA min %d max %d; 10 latest CTAs (exit us, tiles): %s" % (
         tiles.min(), tiles.max(), [(round(ex[i], 1), int(tiles[i])) for i in order[-10:]]))
     print("  10 earliest: %s" % [(round(ex[i], 1), int(tiles[i])) for i in order[:10]])
-    for label, col in (("start", 0), ("first data", 1), ("producer exit", 3)):
+    for label, col in (("start", 0), ("after prologue", 1), ("producer exit", 3)):
         v = rel[:, col]
         v = v[~np.isnan(v)]
         if len(v):
