@@ -82,6 +82,22 @@ def load() -> C.CDLL:
     return lib
 
 
+_EVAL_RAW = None
+
+
+def eval_raw():
+    """musr_eval typed with plain integer pointers: the per-evaluation call
+    from Python is the hot host path, and raw addresses avoid building
+    ctypes pointer objects on every call."""
+    global _EVAL_RAW
+    if _EVAL_RAW is None:
+        lib = load()
+        fn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                         C.c_void_p, C.c_void_p)(("musr_eval", lib))
+        _EVAL_RAW = fn
+    return _EVAL_RAW
+
+
 def nccl_library_path() -> Optional[str]:
     """Path of the torch-bundled libnccl.so.2, if installed."""
     env = os.environ.get("MUSR_NCCL_LIB")
