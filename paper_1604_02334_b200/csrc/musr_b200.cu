@@ -356,6 +356,13 @@ MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   a.bad = c->bad;
   a.out = direct ? c->h_out_dev : c->out_send;
   a.h_inline = c->h_inline ? 1 : 0;
+  if (c->h_inline) {
+    for (int i = 0; i < c->n_local; ++i) {
+      a.hin[i] = c->hist_host[i];
+      for (int k = 0; k < c->map_stride; ++k) a.min[i][k] = c->maps_host[(size_t)i * c->map_stride + k];
+      for (int k = 0; k < c->f_stride; ++k) a.fin[i][k] = c->fvals_host[(size_t)i * c->f_stride + k];
+    }
+  }
   a.done_flag = c->flag_dev;
   a.ds_done = c->ds_done;
   a.utab = c->utab;
@@ -451,22 +458,7 @@ int build_graphs(musr_ctx* c) {
   int prc = ensure_utab(c);
   if (prc == MUSR_OK) prc = plan_launch(c);
   if (prc != MUSR_OK) return prc;
-  if (c->h_inline) {  // small-problem metadata -> the module's constant bank
-    MusrMetaConst meta;
-    std::memset(&meta, 0, sizeof(meta));
-    for (int i = 0; i < c->n_local; ++i) {
-      meta.hin[i] = c->hist_host[i];
-      for (int k = 0; k < c->map_stride; ++k)
-        meta.min[i][k] = c->maps_host[(size_t)i * c->map_stride + k];
-      for (int k = 0; k < c->f_stride; ++k)
-        meta.fin[i][k] = c->fvals_host[(size_t)i * c->f_stride + k];
-    }
-    CUdeviceptr sym = 0;
-    size_t sym_size = 0;
-    CU_TRY(c, g_drv.ModuleGetGlobal(&sym, &sym_size, c->mod, "musr_meta_c"));
-    if (sym_size != sizeof(meta)) return set_err(c, MUSR_ERR_ARG, "musr_meta_c size mismatch");
-    CUDA_TRY(c, cudaMemcpy((void*)sym, &meta, sizeof(meta), cudaMemcpyHostToDevice));
-  }
+
   for (int kind = 0; kind < 2; ++kind) {
     if (kind == 0 && !c->have_errors) continue;
     cudaGraph_t g = nullptr;

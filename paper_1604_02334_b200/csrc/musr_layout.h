@@ -55,13 +55,10 @@ struct MusrArgs {
   unsigned int* ds_done;      // datasets completed in this launch (self-resetting)
   unsigned long long epoch;   // evaluation sequence number (direct path), 0 = no flag
   int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
-  int h_inline;               // 1: musr_meta_c holds all datasets' metadata
+  int h_inline;               // 1: hin/min/fin hold all datasets' metadata
   double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)
-};
-
-// Small-problem metadata in the module's constant bank (written at upload):
-// the CTA prologue then reads no global memory.
-struct MusrMetaConst {
+  // Small-problem metadata inline in the kernel parameters: they arrive with
+  // the launch, so the CTA prologue issues no dependent global/constant misses.
   MusrHist hin[MUSR_H_INLINE];
   int min[MUSR_H_INLINE][MUSR_M_INLINE];
   double fin[MUSR_H_INLINE][MUSR_F_INLINE];
