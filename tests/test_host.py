@@ -111,6 +111,35 @@ def test_markstein_division_is_exact(mathlib):
     assert np.array_equal(np.signbit(q[3:]), np.signbit(ref[3:]))
 
 
+def test_device_log_within_one_ulp(mathlib):
+    """musr_log_fast (MLH term) against glibc log, which is correctly rounded here."""
+    import math
+    rng = np.random.default_rng(3)
+    n = 200_000
+    d = rng.integers(1, 5000, n).astype(np.float64)
+    x = np.concatenate([rng.uniform(0.5, 2, n), 1 + rng.uniform(-1e-3, 1e-3, n),
+                        np.exp(rng.uniform(-700, 700, n)), d / rng.uniform(1e-3, 5000, n),
+                        [1.0, 2.0, 0.5, np.nextafter(1.0, 2.0), np.nextafter(1.0, 0.0)]])
+    y = mathlib("v_log", x)
+    ref = np.array([math.log(v) for v in x])
+    assert np.abs(y.view(np.int64) - ref.view(np.int64)).max() <= 1
+    bad = mathlib("v_log", np.array([0.0, -1.0, np.inf, np.nan, 5e-324]))
+    assert np.isnan(bad).all()  # outside the fast domain: the kernel recomputes exactly
+
+
+def test_device_fast_division_is_exact(mathlib):
+    """musr_div_fast (MLH quotient d / m) is the IEEE quotient on its domain."""
+    rng = np.random.default_rng(4)
+    n = 1_000_000
+    for a, b in ((rng.integers(1, 5000, n).astype(np.float64), rng.uniform(1e-3, 5000, n)),
+                 (np.exp(rng.uniform(-340, 340, n)), np.exp(rng.uniform(-340, 340, n)))):
+        q = mathlib("v_div_fast", a, b)
+        assert not np.isnan(q).any()
+        assert np.array_equal(q.view(np.int64), (a / b).view(np.int64))
+    out = mathlib("v_div_fast", np.array([1.0, 0.0, 1e300, 1.0]), np.array([0.0, 1.0, 1.0, -1.0]))
+    assert np.isnan(out).all()
+
+
 # -- error resolution ------------------------------------------------------------
 
 def _ds(j, counts, bmap=(), f=(), n0=0, nbkg=1, t0=0, fit=None):

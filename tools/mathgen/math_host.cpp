@@ -28,4 +28,19 @@ void v_div_y(const double* a, const double* b, const double* yb, double* q, long
   for (long i = 0; i < n; ++i) q[i] = musr_div_y(a[i], b[i], yb[i]);
 }
 
+void v_log(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    y[i] = musr_log_fast(x[i], musr_log_t, ok);
+    if (!ok) y[i] = NAN;
+  }
+}
+void v_div_fast(const double* a, const double* b, double* q, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    q[i] = musr_div_fast(a[i], b[i], ok);
+    if (!ok) q[i] = NAN;
+  }
+}
+
 }  // extern "C"
