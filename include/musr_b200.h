@@ -23,6 +23,10 @@
  *       (musr.py:150-162) and Backend.map_reduce + pairwise_sum
  *       (backend.py:79-95, 174-207).  Returns per-dataset sums, the left-folded
  *       total (musr.py:190-201) and the MLH first non-positive bin per dataset.
+ *   musr_eval_batch
+ *       n_points calls of musr.chi2 / musr.mlh at different p in one pass over
+ *       the histograms (Nelder-Mead simplex / shrink points, optimize.py:89-135;
+ *       profile scans, test_acceptance.py:135-157).
  *   musr_time_evals / musr_fp64_peak
  *       measurement helpers for bench.py (no reference counterpart).
  */
@@ -110,6 +114,17 @@ int musr_upload(musr_ctx* ctx, int n_global, int n_local, const int32_t* out_ind
  * order (may be NULL). */
 int musr_eval(musr_ctx* ctx, int kind, const double* p, int n_p, double* per_dataset,
               int64_t* first_bad_bin, double* total);
+
+/* Batched evaluation: n_points parameter vectors,
+ * row-major in p (n_points x n_p).  Each tile of the histograms is streamed
+ * once per MUSR_KMAX (8) points and evaluated at all of them; larger batches
+ * run in chunks.  Outputs are row-major per point: per_dataset and
+ * first_bad_bin n_points x n_global, totals n_points.  Every point's values are
+ * bit-identical to musr_eval at that point.  Replaces n_points calls of the
+ * reference objective (musr.py:181-232) -- e.g. the Nelder-Mead initial
+ * simplex and shrink steps (optimize.py:89-96, optimize.py:133-135). */
+int musr_eval_batch(musr_ctx* ctx, int kind, const double* p, int n_points, int n_p,
+                    double* per_dataset, int64_t* first_bad_bin, double* totals);
 
 /* Timing helpers (CUDA events on the handle's stream).
  *   mode 0: `iters` back-to-back graph replays (full evaluation incl. H2D p and

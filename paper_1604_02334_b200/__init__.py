@@ -14,6 +14,7 @@ There is no CPU fallback.
 from .musr import (  # noqa: F401
     GAMMA_MU,
     OBJECTIVES,
+    OBJECTIVES_BATCH,
     TAU_MU_US,
     FitResult,
     MusrDataset,
@@ -21,11 +22,13 @@ from .musr import (  # noqa: F401
     ParameterSet,
     PhysicsConstants,
     chi2,
+    chi2_batch,
     default_phases,
     degrees_of_freedom,
     install,
     minimize,
     mlh,
+    mlh_batch,
 )
 from .objective import DeviceBackend, Session, shard_assignment  # noqa: F401
 from .optimize import MinimizeConfig, MinimizeResult, OptimizeError, nelder_mead  # noqa: F401

@@ -47,6 +47,7 @@ SIGNATURES = [
      [C.c_void_p, C.c_int, C.c_int, _I32P, _I64P, _I64P, _I64P, _DP, _VPP, _VPP, _VPP,
       _I32P, _I32P, _I32P, C.c_int, _DP, C.c_int, C.c_int]),
     ("musr_eval", C.c_int, [C.c_void_p, C.c_int, _DP, C.c_int, _DP, _I64P, _DP]),
+    ("musr_eval_batch", C.c_int, [C.c_void_p, C.c_int, _DP, C.c_int, C.c_int, _DP, _I64P, _DP]),
     ("musr_time_evals", C.c_int,
      [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
       C.POINTER(C.c_double)]),

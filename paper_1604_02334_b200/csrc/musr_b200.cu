@@ -156,6 +156,7 @@ struct musr_ctx {
   CUmodule mod = nullptr;
   CUfunction fn[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [kind][fmt]
   CUfunction fn_utab = nullptr;
+  CUfunction fn_batch[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // musr_eval_batch
   bool have_theory = false;
   int n_uniform = 1;            // MUSR_NU of the loaded theory
   int sms = 0;                  // multiprocessors on the device
@@ -169,6 +170,8 @@ struct musr_ctx {
   unsigned* sched = nullptr;    // [2] dynamic tile scheduler (self-resetting)
   unsigned grid[2] = {0, 0};    // persistent grid per kind
   size_t dyn_smem[2] = {0, 0};  // dynamic shared memory per kind
+  unsigned grid_batch[2] = {0, 0};
+  size_t dyn_smem_batch[2] = {0, 0};
   int per_thread_data = 8;      // per_thread the uploaded layout was padded for
 
   // data
@@ -195,6 +198,9 @@ struct musr_ctx {
   double* out_send = nullptr;
   double* out_recv = nullptr;
   double* h_p = nullptr;    // pinned
+  double* P_batch = nullptr;    // [MUSR_KMAX][p_capacity] (musr_eval_batch)
+  double* h_p_batch = nullptr;  // pinned staging of P_batch
+  double* h_out_batch = nullptr;  // pinned, [MUSR_KMAX][2 * n_global]
   double* h_out = nullptr;  // pinned + mapped, 2 * n_global
   double* h_out_dev = nullptr;  // device alias of h_out (direct path writes here)
   std::vector<double> last_p;   // parameter vector of the last evaluation (timing replays)
@@ -302,7 +308,7 @@ void free_data(musr_ctx* c) {
   free_graphs(c);
   void* dev[] = {c->d, c->e, c->rcp, c->env, c->table, c->tile_hist, c->hist, c->P, c->maps,
                  c->fvals, c->partial, c->count, c->bad, c->out_send, c->out_recv, c->utab,
-                 c->sched, c->ds_done};
+                 c->sched, c->ds_done, c->P_batch};
   for (void* p : dev)
     if (p) cudaFree(p);
   c->d = nullptr;
@@ -322,6 +328,10 @@ void free_data(musr_ctx* c) {
   c->utab_rows = 0;
   c->sched = nullptr;
   c->ds_done = nullptr;
+  c->P_batch = nullptr;
+  if (c->h_p_batch) cudaFreeHost(c->h_p_batch);
+  if (c->h_out_batch) cudaFreeHost(c->h_out_batch);
+  c->h_p_batch = c->h_out_batch = nullptr;
   if (c->flag_host) cudaFreeHost(c->flag_host);
   c->flag_host = c->flag_dev = nullptr;
   if (c->h_p) cudaFreeHost(c->h_p);
@@ -371,6 +381,8 @@ MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   a.n_tiles = (int)c->n_tiles;
   a.n_global = c->n_global;
   a.n_local = c->n_local;
+  a.n_points = 1;
+  a.p_stride = c->p_capacity;
   return a;
 }
 
@@ -432,6 +444,23 @@ int plan_launch(musr_ctx* c) {
     if (occ < 1) return set_err(c, MUSR_ERR_CUDA, "objective kernel does not fit on an SM");
     const int64_t cap = (int64_t)c->sms * occ;
     c->grid[kind] = (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, cap));
+
+    // batched variant: rows come from the global table; the per-point thread
+    // nodes take the place of the staged rows (musr_kernel.cuh: s_tn)
+    size_t smem_b = (size_t)stages * stage;
+    if (kind == 0 && c->fmt == 1) smem_b += (size_t)c->table_size * 16;
+    smem_b += (size_t)stages * MUSR_KMAX * c->cwarps * 33 * sizeof(double);  // [S][KMAX][TN_K * 33]
+    c->dyn_smem_batch[kind] = smem_b;
+    CUfunction fb = c->fn_batch[kind][c->fmt];
+    CU_TRY(c, g_drv.FuncSetAttribute(fb, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                     (int)smem_b));
+    CU_TRY(c, g_drv.FuncSetAttribute(fb, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100));
+    int occ_b = 0;
+    CU_TRY(c, g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, fb, 32 * (c->cwarps + 1),
+                                                               smem_b));
+    if (occ_b < 1) return set_err(c, MUSR_ERR_CUDA, "batched kernel does not fit on an SM");
+    c->grid_batch[kind] =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, (int64_t)c->sms * occ_b));
   }
   if (std::getenv("MUSR_TRACE") && !c->trace) {
     CUDA_TRY(c, cudaMalloc(&c->trace, (size_t)c->sms * 8 * 4 * sizeof(unsigned long long)));
@@ -442,7 +471,7 @@ int plan_launch(musr_ctx* c) {
 
 // Uniform table sized for the loaded theory and data.
 int ensure_utab(musr_ctx* c) {
-  const size_t rows = (size_t)std::max(1, c->n_local) * (size_t)(c->n_uniform + 2);
+  const size_t rows = (size_t)MUSR_KMAX * std::max(1, c->n_local) * (size_t)(c->n_uniform + 2);
   if (c->utab && c->utab_rows >= rows) return MUSR_OK;
   if (c->utab) cudaFree(c->utab);
   c->utab = nullptr;
@@ -733,6 +762,10 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][0], c->mod, "musr_mlh_f64"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][1], c->mod, "musr_mlh_c32"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_utab, c->mod, "musr_uniform_table"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][0], c->mod, "musr_chi2_f64_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][1], c->mod, "musr_chi2_c32_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][0], c->mod, "musr_mlh_f64_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][1], c->mod, "musr_mlh_c32_batch"));
   c->have_theory = true;
   return build_graphs(c);
 }
@@ -849,13 +882,14 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   ALLOC(c->P, (size_t)p_capacity * 8);
   ALLOC(c->maps, (size_t)n_local * map_stride * 4);
   ALLOC(c->fvals, (size_t)n_local * f_stride * 8);
-  ALLOC(c->partial, (size_t)tiles * 8);
+  ALLOC(c->partial, (size_t)MUSR_KMAX * tiles * 8);
   ALLOC(c->count, (size_t)n_local * 4);
   ALLOC(c->sched, 2 * sizeof(unsigned));
   ALLOC(c->ds_done, sizeof(unsigned));
-  ALLOC(c->bad, (size_t)n_local * 8);
-  ALLOC(c->out_send, (size_t)2 * n_global * 8);
-  ALLOC(c->out_recv, (size_t)2 * n_global * 8);
+  ALLOC(c->bad, (size_t)MUSR_KMAX * n_local * 8);
+  ALLOC(c->out_send, (size_t)MUSR_KMAX * 2 * n_global * 8);
+  ALLOC(c->out_recv, (size_t)MUSR_KMAX * 2 * n_global * 8);
+  ALLOC(c->P_batch, (size_t)MUSR_KMAX * p_capacity * 8);
 #undef ALLOC
   if (cudaHostAlloc((void**)&c->h_p, (size_t)p_capacity * 8, cudaHostAllocDefault) !=
           cudaSuccess ||
@@ -864,7 +898,11 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
       cudaHostGetDevicePointer((void**)&c->h_out_dev, c->h_out, 0) != cudaSuccess ||
       cudaHostAlloc((void**)&c->flag_host, sizeof(unsigned long long), cudaHostAllocMapped) !=
           cudaSuccess ||
-      cudaHostGetDevicePointer((void**)&c->flag_dev, c->flag_host, 0) != cudaSuccess) {
+      cudaHostGetDevicePointer((void**)&c->flag_dev, c->flag_host, 0) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->h_p_batch, (size_t)MUSR_KMAX * p_capacity * 8,
+                    cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void**)&c->h_out_batch, (size_t)MUSR_KMAX * 2 * n_global * 8,
+                    cudaHostAllocDefault) != cudaSuccess) {
     free_data(c);
     return set_err(c, MUSR_ERR_NOMEM, "pinned host allocation failed");
   }
@@ -928,9 +966,9 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   CUDA_TRY(c, cudaMemset(c->ds_done, 0, sizeof(unsigned)));
   *c->flag_host = 0;
   c->epoch = 0;
-  CUDA_TRY(c, cudaMemset(c->bad, 0xff, (size_t)n_local * 8));
-  CUDA_TRY(c, cudaMemset(c->out_send, 0, (size_t)2 * n_global * 8));
-  CUDA_TRY(c, cudaMemset(c->out_recv, 0, (size_t)2 * n_global * 8));
+  CUDA_TRY(c, cudaMemset(c->bad, 0xff, (size_t)MUSR_KMAX * n_local * 8));
+  CUDA_TRY(c, cudaMemset(c->out_send, 0, (size_t)MUSR_KMAX * 2 * n_global * 8));
+  CUDA_TRY(c, cudaMemset(c->out_recv, 0, (size_t)MUSR_KMAX * 2 * n_global * 8));
   c->have_data = true;
   return build_graphs(c);
 }
@@ -1036,6 +1074,73 @@ int musr_format(const musr_ctx* c, int* format, int* table_size) {
 int musr_tiles(const musr_ctx* c, int64_t* n_tiles) {
   if (!c || !n_tiles) return MUSR_ERR_ARG;
   *n_tiles = c->n_tiles;
+  return MUSR_OK;
+}
+
+// Batched evaluation: up to MUSR_KMAX parameter vectors per launch pair
+// (uniform table over points x datasets, then one pass over the tiles that
+// evaluates every point), larger batches in chunks.  Each point's results are
+// bit-identical to musr_eval at that point.
+int musr_eval_batch(musr_ctx* c, int kind, const double* p, int n_points, int n_p,
+                    double* per_dataset, int64_t* first_bad_bin, double* totals) {
+  if (!c) return set_err(c, MUSR_ERR_ARG, "NULL handle");
+  if (kind != MUSR_KIND_CHI2 && kind != MUSR_KIND_MLH)
+    return set_err(c, MUSR_ERR_ARG, fmt("unknown objective kind %d", kind));
+  if (!c->have_theory || !c->have_data)
+    return set_err(c, MUSR_ERR_ARG, "theory and data must be set before musr_eval_batch");
+  if (!c->gexec[kind])
+    return set_err(c, MUSR_ERR_ARG, "chi2 needs the error histograms (upload errors)");
+  if (n_points < 0) return set_err(c, MUSR_ERR_ARG, "negative n_points");
+  if (n_p < 0 || n_p > c->p_capacity)
+    return set_err(c, MUSR_ERR_ARG, fmt("parameter vector length %d exceeds capacity %d", n_p,
+                                        c->p_capacity));
+  if (n_points && n_p && !p) return set_err(c, MUSR_ERR_ARG, "p is NULL");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int G = c->n_global, cap = c->p_capacity;
+  for (int base = 0; base < n_points; base += MUSR_KMAX) {
+    const int K = std::min(MUSR_KMAX, n_points - base);
+    std::memset(c->h_p_batch, 0, (size_t)K * cap * 8);
+    for (int k = 0; k < K; ++k)
+      if (n_p) std::memcpy(c->h_p_batch + (size_t)k * cap, p + (size_t)(base + k) * n_p,
+                           (size_t)n_p * 8);
+    CUDA_TRY(c, cudaMemcpyAsync(c->P_batch, c->h_p_batch, (size_t)K * cap * 8,
+                                cudaMemcpyHostToDevice, c->stream));
+    if (c->n_tiles > 0) {
+      MusrArgs a = make_args(c, false);
+      a.P = c->P_batch;
+      a.p_stride = cap;
+      a.p_inline = 0;
+      a.n_points = K;
+      a.epoch = 0;
+      void* params[] = {&a};
+      const unsigned rows = (unsigned)(K * c->n_local);
+      CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (rows + 127) / 128, 1, 1, 128, 1, 1, 0,
+                                   (CUstream)c->stream, params, nullptr));
+      CU_TRY(c, g_drv.LaunchKernel(c->fn_batch[kind][c->fmt], c->grid_batch[kind], 1, 1,
+                                   32 * (c->cwarps + 1), 1, 1, (unsigned)c->dyn_smem_batch[kind],
+                                   (CUstream)c->stream, params, nullptr));
+    }
+    if (c->comm) {
+      const int nr = g_nccl.AllReduce(c->out_send, c->out_recv, (size_t)K * 2 * G, kNcclFloat64,
+                                      kNcclSum, c->comm, c->stream);
+      if (nr != 0)
+        return set_err(c, MUSR_ERR_NCCL, fmt("ncclAllReduce: %s", g_nccl.GetErrorString(nr)));
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_out_batch, c->comm ? c->out_recv : c->out_send,
+                                (size_t)K * 2 * G * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < K; ++k) {
+      const double* o = c->h_out_batch + (size_t)k * 2 * G;
+      const size_t row = (size_t)(base + k) * G;
+      double acc = 0.0;
+      for (int i = 0; i < G; ++i) {
+        if (per_dataset) per_dataset[row + i] = o[i];
+        if (first_bad_bin) first_bad_bin[row + i] = (o[G + i] == 0.0) ? -1 : (int64_t)o[G + i] - 1;
+        acc = acc + o[i];  // musr.py:190-201, per point
+      }
+      if (totals) totals[base + k] = acc;
+    }
+  }
   return MUSR_OK;
 }
 

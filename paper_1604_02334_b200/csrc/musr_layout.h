@@ -13,6 +13,8 @@
 #define MUSR_H_INLINE 16
 #define MUSR_M_INLINE 12
 #define MUSR_F_INLINE 4
+// Batched evaluation (musr_eval_batch): parameter vectors per objective launch.
+#define MUSR_KMAX 8
 
 struct MusrHist {
   long long n_terms;    // in-range bins
@@ -40,11 +42,11 @@ struct MusrArgs {
   const double* P;            // parameter vector
   const int* maps;            // map rows
   const double* fvals;        // function-value rows
-  double* partial;            // [n_tiles] tile nodes
+  double* partial;            // [n_points][n_tiles] tile nodes
   unsigned int* count;        // [n_local] tiles finished (self-resetting)
-  unsigned long long* bad;    // [n_local] first non-positive bin (self-resetting)
-  double* out;                // [2 * n_global]: sums | (bad bin + 1), 0 = none
-  double* utab;               // [n_local][MUSR_NU + 2] uniform values, N0, Nbkg
+  unsigned long long* bad;    // [n_points][n_local] first non-positive bin (self-resetting)
+  double* out;                // [n_points][2 * n_global]: sums | (bad bin + 1), 0 = none
+  double* utab;               // [n_points][n_local][MUSR_NU + 2] uniform values, N0, Nbkg
   int n_global;               // datasets over all ranks
   int n_local;                // datasets on this device
   int n_tiles;                // tiles on this device
@@ -54,6 +56,8 @@ struct MusrArgs {
   unsigned long long* done_flag;  // direct path: mapped host word, set to `epoch` when done
   unsigned int* ds_done;      // datasets completed in this launch (self-resetting)
   unsigned long long epoch;   // evaluation sequence number (direct path), 0 = no flag
+  int n_points;               // parameter vectors in this launch (1, or <= MUSR_KMAX batched)
+  int p_stride;               // batched: P holds n_points rows of p_stride doubles
   int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
   int h_inline;               // 1: hin/min/fin hold all datasets' metadata
   double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)

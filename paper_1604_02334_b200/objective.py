@@ -375,6 +375,43 @@ class Session:
             raise _fresh(static[1])
         return float(self._total[0])
 
+    def evaluate_batch(self, kind: int, P, musr_error: type = None) -> np.ndarray:
+        """Objective values at every row of ``P`` (n_points x n_p) from one
+        pass over the histograms per MUSR_KMAX points (musr_eval_batch).  Row i
+        equals ``evaluate(kind, P[i])`` bit for bit; if any row would raise,
+        the exception of the first such row (in row order) is raised."""
+        P = np.ascontiguousarray(P, dtype=np.float64)
+        if P.ndim != 2 or P.shape[1] != self.n_p:
+            raise ValueError("P must be (n_points, n_p) with the session's n_p")
+        n = P.shape[0]
+        if n == 0:
+            return np.zeros(0, dtype=np.float64)
+        static = self.first_static
+        if static is not None and (static[0] == 0 or self.total_terms == 0):
+            raise _fresh(static[1])
+        sums = np.empty((n, self.n_global), dtype=np.float64)
+        bad = np.empty((n, self.n_global), dtype=np.int64)
+        tot = np.empty(n, dtype=np.float64)
+        dp = C.POINTER(C.c_double)
+        _lib.check(self._lib.musr_eval_batch(
+            self._handle, kind, P.ctypes.data_as(dp), n, self.n_p, sums.ctypes.data_as(dp),
+            bad.ctypes.data_as(C.POINTER(C.c_int64)), tot.ctypes.data_as(dp)),
+            self._handle, "musr_eval_batch")
+        if kind == _lib.KIND_MLH:
+            for i in range(n):       # first failing point, then its first failing dataset
+                hit = np.flatnonzero(bad[i] >= 0)
+                if len(hit) and (static is None or hit[0] < static[0]):
+                    j = int(hit[0])
+                    det = self._detectors[j] if self._detectors is not None else j
+                    raise (musr_error or ERRORS.musr)(
+                        f"detector {det}: model is non-positive at bin {int(bad[i, j])}")
+                if static is not None:
+                    break
+        if static is not None:
+            raise _fresh(static[1])
+        self._batch_sums = sums
+        return tot
+
     _detectors: Optional[List[int]] = None
 
     def per_dataset(self) -> np.ndarray:

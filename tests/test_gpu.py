@@ -257,3 +257,60 @@ def test_acceptance_criterion_1_fit_recovery():
 
     se = 0.5 * (crossing(+1.0) - crossing(-1.0))
     assert abs(best.values[slot] - 0.05) <= 3.0 * se
+
+
+# -- batched evaluation -----------------------------------------
+
+@pytest.mark.parametrize("name,kw", [("C1", dict(nbins=1 << 14)), ("C2", dict(n_hist=5, nbins=100000)),
+                                     ("C3", dict(n_hist=3, nbins=70001))])
+def test_batch_bitwise_equals_single(name, kw):
+    """Every row of chi2_batch / mlh_batch equals the scalar call bit for bit,
+    across chunk boundaries (MUSR_KMAX = 8 points per launch)."""
+    w = workloads.WORKLOADS[name](**kw)
+    dss = workloads.synthesize(w)
+    rng = np.random.default_rng(11)
+    for n_points in (1, 3, 8, 13):
+        P = w.params * (1.0 + 0.02 * rng.standard_normal((n_points, len(w.params))))
+        for kind, one, many in (("chi2", pkg.chi2, pkg.chi2_batch), ("mlh", pkg.mlh, pkg.mlh_batch)):
+            got = many(dss, w.expr, P)
+            want = np.array([one(dss, w.expr, p) for p in P])
+            assert got.shape == (n_points,)
+            assert np.array_equal(got.view(np.int64), want.view(np.int64)), (name, kind, n_points)
+    assert pkg.chi2_batch(dss, w.expr, np.zeros((0, len(w.params)))).shape == (0,)
+
+
+def test_batch_many_datasets_and_collective_path():
+    w = workloads.c4(n_hist=70, nbins=2000)            # > 64 datasets: unstaged metadata
+    dss = workloads.synthesize(w)
+    P = np.repeat(w.params[None, :], 9, axis=0)
+    P[:, 1] *= np.linspace(0.9, 1.1, 9)
+    want = np.array([pkg.chi2(dss, w.expr, p) for p in P])
+    assert np.array_equal(pkg.chi2_batch(dss, w.expr, P), want)
+    be = pkg.DeviceBackend(collective=True, nccl_id=objective.new_nccl_id())
+    assert np.array_equal(pkg.chi2_batch(dss, w.expr, P, be), want)
+
+
+def test_batch_mlh_error_is_first_failing_point():
+    expr = pkg.parse("p[m[0]] * t")
+    ds = pkg.MusrDataset(3, np.full(50000, 50), 0.001, 11, pkg.TheoryBinding(map=(2,)), 0, 1)
+    good = np.array([1.0, 0.0, 0.0])
+    bad1 = np.array([1.0, 0.0, -1.0 / 30.0])
+    bad2 = np.array([1.0, 0.0, -1.0 / 20.0])
+    with pytest.raises(pkg.MusrError) as exc:
+        pkg.mlh_batch([ds], expr, np.array([good, bad2, bad1]))
+    with pytest.raises(pkg.MusrError) as one:
+        pkg.mlh([ds], expr, bad2)
+    assert str(exc.value) == str(one.value)
+    assert pkg.mlh_batch([ds], expr, np.array([good, good]))[1] == pkg.mlh([ds], expr, good)
+
+
+def test_minimize_batched_simplex_identical_to_unbatched():
+    """minimize() batches the initial simplex and shrink points; the fit is
+    bit-identical to the one-call-per-point loop."""
+    dss, expr, start = _eq6_problem(4, 20000, 7, 0.0005)
+    batched = pkg.minimize("chi2", dss, expr, start)
+    single = pkg.minimize("chi2", dss, expr, start,
+                          objective_fn=lambda p: pkg.chi2(dss, expr, p))
+    assert np.array_equal(batched.best_parameters.values, single.best_parameters.values)
+    assert batched.objective_value == single.objective_value
+    assert batched.objective_evaluations == single.objective_evaluations

@@ -267,3 +267,14 @@ def test_nelder_mead_identical_to_reference(ref):
             b = ref.optimize.nelder_mead(fn, x0, st, lo, hi, ref.optimize.MinimizeConfig(**cfg_args))
             assert np.array_equal(a.x, b.x) and a.fun == b.fun
             assert (a.iterations, a.evaluations, a.converged) == (b.iterations, b.evaluations, b.converged)
+            # the batched simplex / shrink path (fn_batch) takes the same decisions
+            calls = []
+
+            def fb(X, fn=fn):
+                calls.append(len(X))
+                return np.array([fn(x) for x in X])
+
+            c = nelder_mead(fn, x0, st, lo, hi, MinimizeConfig(**cfg_args), fb)
+            assert np.array_equal(c.x, b.x) and c.fun == b.fun
+            assert (c.iterations, c.evaluations, c.converged) == (b.iterations, b.evaluations, b.converged)
+            assert len(x0) == 1 or calls
