@@ -205,9 +205,8 @@ struct musr_ctx {
   double* h_out_dev = nullptr;  // device alias of h_out (direct path writes here)
   std::vector<double> last_p;   // parameter vector of the last evaluation (timing replays)
   MusrArgs direct_args;         // prebuilt direct-launch arguments (only pin[]/epoch change)
-  unsigned long long* flag_host = nullptr;  // mapped completion word (direct path)
-  unsigned long long* flag_dev = nullptr;
-  unsigned* ds_done = nullptr;
+  unsigned long long* ll_host = nullptr;  // mapped LL result words (direct path), 4 per dataset
+  unsigned long long* ll_dev = nullptr;
   unsigned long long epoch = 0;
   bool direct_args_ok = false;
   bool h_inline = false;        // metadata small enough for kernel-parameter space
@@ -308,7 +307,7 @@ void free_data(musr_ctx* c) {
   free_graphs(c);
   void* dev[] = {c->d, c->e, c->rcp, c->env, c->table, c->tile_hist, c->hist, c->P, c->maps,
                  c->fvals, c->partial, c->count, c->bad, c->out_send, c->out_recv, c->utab,
-                 c->sched, c->ds_done, c->P_batch};
+                 c->sched, c->P_batch};
   for (void* p : dev)
     if (p) cudaFree(p);
   c->d = nullptr;
@@ -327,13 +326,12 @@ void free_data(musr_ctx* c) {
   c->utab = nullptr;
   c->utab_rows = 0;
   c->sched = nullptr;
-  c->ds_done = nullptr;
   c->P_batch = nullptr;
   if (c->h_p_batch) cudaFreeHost(c->h_p_batch);
   if (c->h_out_batch) cudaFreeHost(c->h_out_batch);
   c->h_p_batch = c->h_out_batch = nullptr;
-  if (c->flag_host) cudaFreeHost(c->flag_host);
-  c->flag_host = c->flag_dev = nullptr;
+  if (c->ll_host) cudaFreeHost(c->ll_host);
+  c->ll_host = c->ll_dev = nullptr;
   if (c->h_p) cudaFreeHost(c->h_p);
   if (c->h_out) cudaFreeHost(c->h_out);
   c->h_p = c->h_out = nullptr;
@@ -373,8 +371,7 @@ MusrArgs make_args(const musr_ctx* c, bool direct = false) {
       for (int k = 0; k < c->f_stride; ++k) a.fin[i][k] = c->fvals_host[(size_t)i * c->f_stride + k];
     }
   }
-  a.done_flag = c->flag_dev;
-  a.ds_done = c->ds_done;
+  a.ll = c->ll_dev;
   a.utab = c->utab;
   a.trace = c->trace;
   a.sched = c->sched;
@@ -885,7 +882,6 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   ALLOC(c->partial, (size_t)MUSR_KMAX * tiles * 8);
   ALLOC(c->count, (size_t)n_local * 4);
   ALLOC(c->sched, 2 * sizeof(unsigned));
-  ALLOC(c->ds_done, sizeof(unsigned));
   ALLOC(c->bad, (size_t)MUSR_KMAX * n_local * 8);
   ALLOC(c->out_send, (size_t)MUSR_KMAX * 2 * n_global * 8);
   ALLOC(c->out_recv, (size_t)MUSR_KMAX * 2 * n_global * 8);
@@ -896,9 +892,9 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
       cudaHostAlloc((void**)&c->h_out, (size_t)2 * n_global * 8, cudaHostAllocMapped) !=
           cudaSuccess ||
       cudaHostGetDevicePointer((void**)&c->h_out_dev, c->h_out, 0) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->flag_host, sizeof(unsigned long long), cudaHostAllocMapped) !=
+      cudaHostAlloc((void**)&c->ll_host, (size_t)4 * n_global * 8, cudaHostAllocMapped) !=
           cudaSuccess ||
-      cudaHostGetDevicePointer((void**)&c->flag_dev, c->flag_host, 0) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->ll_dev, c->ll_host, 0) != cudaSuccess ||
       cudaHostAlloc((void**)&c->h_p_batch, (size_t)MUSR_KMAX * p_capacity * 8,
                     cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc((void**)&c->h_out_batch, (size_t)MUSR_KMAX * 2 * n_global * 8,
@@ -963,8 +959,8 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   }
   CUDA_TRY(c, cudaMemset(c->count, 0, (size_t)n_local * 4));
   CUDA_TRY(c, cudaMemset(c->sched, 0, 2 * sizeof(unsigned)));
-  CUDA_TRY(c, cudaMemset(c->ds_done, 0, sizeof(unsigned)));
-  *c->flag_host = 0;
+  std::memset(c->ll_host, 0, (size_t)4 * n_global * 8);
+  std::memset(c->h_out, 0, (size_t)2 * n_global * 8);
   c->epoch = 0;
   CUDA_TRY(c, cudaMemset(c->bad, 0xff, (size_t)MUSR_KMAX * n_local * 8));
   CUDA_TRY(c, cudaMemset(c->out_send, 0, (size_t)MUSR_KMAX * 2 * n_global * 8));
@@ -1023,22 +1019,45 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
   c->last_p.assign(p, p + n_p);
   static const bool no_flag = std::getenv("MUSR_NO_FLAG") != nullptr;
   const bool flagged = direct_mode(c) && c->n_tiles > 0 && !no_flag;
-  if (flagged) c->epoch += 1;
+  if (flagged) {
+    c->epoch += 1;
+    if ((uint32_t)c->epoch == 0) c->epoch += 1;  // 0 marks "never written"
+  }
   int rc = launch_eval(c, kind, flagged ? c->epoch : 0);
   if (rc != MUSR_OK) return rc;
+  const int G = c->n_global;
   if (flagged) {
-    // The last dataset's writer raises the mapped flag after its results are
-    // visible (system fence); polling it returns ~µs earlier than a stream
-    // sync.  Bounded: after ~20 ms fall back to the sync, which reports errors.
-    volatile unsigned long long* flag = c->flag_host;
-    for (long spin = 0; *flag != c->epoch; ++spin) {
-      if (spin > (1L << 22)) break;
+    // Each local dataset's stage-2 writer stores its results as LL words
+    // carrying this evaluation's epoch; the host reads them as they land
+    // (no completion flag, no device-side fence), typically before the kernel
+    // has retired.  Bounded: after ~20 ms a stream sync (which reports
+    // errors), after which every word is current.
+    const uint32_t e32 = (uint32_t)c->epoch;
+    volatile unsigned long long* ll = c->ll_host;
+    int i = 0, w = 0;
+    for (long spin = 0; i < c->n_local && spin <= (1L << 22); ++spin) {
+      const int o = c->hist_host[i].out_index;
+      while (w < 4 && (uint32_t)ll[4 * o + w] == e32) ++w;
+      if (w == 4) { ++i; w = 0; }
     }
-    if (*flag != c->epoch) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (i < c->n_local) {
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      for (int j = 0; j < c->n_local; ++j)
+        for (int q = 0; q < 4; ++q)
+          if ((uint32_t)ll[4 * c->hist_host[j].out_index + q] != e32)
+            return set_err(c, MUSR_ERR_CUDA, "evaluation finished without its results");
+    }
+    for (int j = 0; j < c->n_local; ++j) {
+      const int o = c->hist_host[j].out_index;
+      const unsigned long long* x = (const unsigned long long*)ll + 4 * o;
+      const unsigned long long s = ((x[0] >> 32) << 32) | (x[1] >> 32);
+      const unsigned long long b = ((x[2] >> 32) << 32) | (x[3] >> 32);
+      std::memcpy(&c->h_out[o], &s, 8);
+      std::memcpy(&c->h_out[G + o], &b, 8);
+    }
   } else {
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   }
-  const int G = c->n_global;
   double acc = 0.0;
   for (int i = 0; i < G; ++i) {
     const double s = c->h_out[i];

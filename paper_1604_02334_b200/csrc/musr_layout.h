@@ -53,9 +53,12 @@ struct MusrArgs {
   int table_size;             // entries of `table` (c32 format)
   unsigned long long* trace;  // MUSR_TRACE builds: per-CTA %globaltimer stamps
   unsigned int* sched;        // [2] dynamic tile scheduler: next tile, exited CTAs (self-resetting)
-  unsigned long long* done_flag;  // direct path: mapped host word, set to `epoch` when done
-  unsigned int* ds_done;      // datasets completed in this launch (self-resetting)
-  unsigned long long epoch;   // evaluation sequence number (direct path), 0 = no flag
+  // Direct path: results go to mapped host memory as "LL" words -- each
+  // 32-bit half of a result travels with the evaluation's 32-bit epoch in one
+  // 8-byte store ((half << 32) | epoch), so the host knows a word is current
+  // without any fence or completion flag.  [n_global][4]: sum hi, lo, bad hi, lo.
+  unsigned long long* ll;
+  unsigned long long epoch;   // evaluation sequence number (direct path), 0 = write `out`
   int n_points;               // parameter vectors in this launch (1, or <= MUSR_KMAX batched)
   int p_stride;               // batched: P holds n_points rows of p_stride doubles
   int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
