@@ -47,6 +47,8 @@ extern "C" {
 #define MUSR_ERR_NCCL 4     /* NCCL failure (sharded handles)            */
 #define MUSR_ERR_NOMEM 5    /* device or pinned allocation failed        */
 
+#define MUSR_ERR_IO 6       /* muSR data file: see musr_io_error.code     */
+
 #define MUSR_KIND_CHI2 0
 #define MUSR_KIND_MLH 1
 
@@ -154,6 +156,61 @@ int musr_debug_trace(musr_ctx* ctx, int kind, uint64_t* out, int cap, int* n_cta
 
 /* DFMA throughput probe: returns measured fp64 TFLOP/s (2 flops per DFMA). */
 int musr_fp64_peak(int device, double* tflops);
+
+/* ---- muSR data file (fast ingest) --------------------
+ * Native, multi-threaded reader / writer of the reference's text format
+ * (pkg/src/blk/io.py:109-140 store_musr_data, io.py:143-212 load_musr_data),
+ * replacing both.  The reader reproduces load_musr_data's decisions line by
+ * line; on failure it reports which error the reference raises first, and
+ * where, and the caller formats the reference's message from it
+ * (paper_1604_02334_b200/musrio.py). */
+#define MUSR_IO_OS 1             /* open/read/write failed; errno in `bin`          */
+#define MUSR_IO_MALFORMED 2      /* "{path}:{line}: malformed line: {text!r}"       */
+#define MUSR_IO_BEFORE_HEADER 3  /* "{path}:{line}: data before any DETECTOR header" */
+#define MUSR_IO_UNKNOWN_KEY 4    /* "{path}:{line}: unknown key {first token!r}"    */
+#define MUSR_IO_MISSING 5        /* "{path}: detector {d} is missing {missing}"     */
+#define MUSR_IO_NEGATIVE 6       /* "{path}: detector {d} has a negative count at bin {bin}" */
+#define MUSR_IO_BAD_MAP 7        /* TheoryError "map entries must be non-negative integers" */
+#define MUSR_IO_EMPTY_HIST 8     /* "{path}: detector {d}: empty histogram"         */
+#define MUSR_IO_BAD_DT 9         /* "{path}: detector {d}: dt must be positive"     */
+#define MUSR_IO_NO_BLOCKS 10     /* "{path}: no detector blocks found"              */
+#define MUSR_IO_UNSUPPORTED 11   /* non-ASCII bytes or integers beyond int64: the
+                                    caller parses the file with the Python rules   */
+typedef struct musr_io_error {
+  int code;
+  int64_t line;       /* 1-based line of a line error, else -1                     */
+  int64_t text_off;   /* byte offset / length of that (stripped) line in the file  */
+  int64_t text_len;
+  int64_t detector;   /* DETECTOR index of a block error, else -1                  */
+  int64_t bin;        /* negative-count bin, or errno for MUSR_IO_OS              */
+  char missing[96];   /* MUSR_IO_MISSING: "dt, t0, ..." in the reference's order  */
+} musr_io_error;
+
+typedef struct musr_file musr_file;
+typedef struct musr_detector_info {
+  int64_t index;      /* DETECTOR value                                             */
+  double dt;
+  int64_t t0_bin, n0_slot, nbkg_slot;
+  int64_t n_map, n_func, n_counts;
+} musr_detector_info;
+
+/* Parse a muSR data file with `n_threads` threads (<= 0: all cores). */
+int musr_file_load(const char* path, int n_threads, musr_file** out, musr_io_error* err);
+int musr_file_n_detectors(const musr_file* f);
+int musr_file_detector(const musr_file* f, int i, musr_detector_info* info);
+/* Copy detector i's map (int64), func (double) and counts (as float64 like
+ * MusrDataset.counts, and/or int64); any pointer may be NULL. */
+int musr_file_copy(const musr_file* f, int i, int64_t* map, double* func, double* counts_f64,
+                   int64_t* counts_i64);
+void musr_file_free(musr_file* f);
+
+/* Write a muSR data file: headers[d] is detector d's "DETECTOR ... func ..."
+ * text (one '\n'-terminated line per key, formatted like store_musr_data);
+ * its counts are truncated to int64 (ndarray.astype) and written 16 per line,
+ * detectors separated by an empty line, exactly as store_musr_data. */
+int musr_file_store(const char* path, int n_det, const char* const* headers,
+                    const double* const* counts, const int64_t* n_counts, int n_threads,
+                    musr_io_error* err);
 
 #ifdef __cplusplus
 }
