@@ -77,12 +77,14 @@ class StaticEvent:
 @dataclass
 class Lowered:
     source: str                 # CUDA fragment (musr_uniform + musr_theory)
-    n_uniform: int              # MUSR_NU
+    n_uniform: int              # MUSR_NU: row length (uniform values + rotation tables)
     uniform_exprs: List[str]    # readable form of each U slot (docs / debugging)
     events: List[StaticEvent]   # postfix-ordered raise points
     max_p_slot: int             # largest k in p[m[k]] (-1 if none)
     max_f_slot: int             # largest k in f[m[k]] (-1 if none)
     per_bin: bool               # does A depend on t at all
+    n_uniform_reg: int = 1      # MUSR_NU_REG: leading row entries kept in registers
+    n_rotations: int = 0        # MUSR_NROT: rotated cos/sin arguments
 
 
 # -- static events + literal folding on the user AST --------------------------
@@ -289,16 +291,28 @@ class _VecEmitter:
     exp and bin-uniform-exponent pow are *anchored* on the run's first bin
     (csrc/musr_math.cuh: musr_exp_anchored / musr_pow_anchored): one full
     evaluation per run plus a short series per further bin, with the error
-    bounded per bin (no accumulation).  cos/sin use the fast per-bin form.
+    bounded per bin (no accumulation).
+
+    cos/sin of an argument affine in t with uniform coefficients,
+    ``a(t) = W*t (+/- Phi)`` -- the ``tf`` precession -- are *rotated*: the
+    argument a_j of every bin is computed exactly as the reference does, the
+    run's first bin gets one full sincos (c0, s0), and bin j uses the
+    per-dataset table (D_j = W*(j*dt), cos D_j, sin D_j) built with the
+    uniform row:  cos(a_j) = C_j - S_j*e_j,  sin(a_j) = S_j + C_j*e_j, with
+    C_j + i S_j = (c0 + i s0)(cos D_j + i sin D_j) and e_j = (a_j - a_0) - D_j
+    (|e_j| ~ ulp(a), so the dropped e_j^2 term is < 2^-62).  Per bin 7 FP64
+    operations instead of a reduction and a degree-8 polynomial; the error
+    stays bounded per bin (every run restarts from an evaluated anchor).
     Any argument outside a fast form's window clears ``ok``.
     """
 
-    def __init__(self, scalar_leaf, uniform_of):
+    def __init__(self, scalar_leaf, uniform_of, rotations=None):
         self.lines: List[str] = []
         self.names: Dict[Node, str] = {}
         self.scalar_leaf = scalar_leaf   # uniform node -> C expression (U[k] / literal)
         self.uniform_of = uniform_of
         self.n = 0
+        self.rotations = rotations       # {arg node: table index}, None = no rotation
 
     def _fresh(self) -> str:
         self.n += 1
@@ -344,12 +358,31 @@ class _VecEmitter:
                 raise TheoryError("uniform exp reached the vector emitter")
             self.lines.append(f"  {name}[0] = musr_exp_fast({x}[0], ok);")
             self._loop(name, f"musr_exp_anchored({x}[j], {x}[0], {name}[0], ok)", first=1)
+        elif node.name in ("cos", "sin") and self.rotations is not None and arg in self.rotations:
+            self._rotated(name, node.name, arg, self.rotations[arg])
         elif node.name in ("cos", "sin"):
             self._loop(name, f"musr_{node.name}_fast({self.ref(arg, 'j')}, ok)")
         elif node.name == "sqrt":
             self._loop(name, f"__dsqrt_rn({self.ref(arg, 'j')})")
         else:
             self._loop(name, f"{_FUNC_EXACT[node.name]}({self.ref(arg, 'j')})")
+
+    def _rotated(self, name: str, fn: str, arg: Node, r: int) -> None:
+        a = self.vec(arg)
+        tab = f"(R + MUSR_NU_REG + {3 * (ROT_TABLE + 1) * r})"
+        out = "__fma_rn(-S_, e_, C_)" if fn == "cos" else "__fma_rn(C_, e_, S_)"
+        self.lines.append(f"  {{ double s0_, c0_;")
+        self.lines.append(f"    musr_sincos_fast({a}[0], &s0_, &c0_, ok);")
+        self.lines.append(f"    {name}[0] = {'c0_' if fn == 'cos' else 's0_'};")
+        self.lines.append(f"    #pragma unroll")
+        self.lines.append(f"    for (int j = 1; j < MUSR_PT; ++j) {{")
+        self.lines.append(f"      const double* tb_ = {tab} + 3 * j;")
+        self.lines.append(f"      const double e_ = __dsub_rn(__dsub_rn({a}[j], {a}[0]), tb_[0]);")
+        self.lines.append(f"      ok = ok && musr_abs_below(e_, 0x3e000000);  // |e| < 2^-31")
+        self.lines.append(f"      const double C_ = __fma_rn(c0_, tb_[1], -__dmul_rn(s0_, tb_[2]));")
+        self.lines.append(f"      const double S_ = __fma_rn(s0_, tb_[1], __dmul_rn(c0_, tb_[2]));")
+        self.lines.append(f"      {name}[j] = {out};")
+        self.lines.append(f"    }} }}")
 
     def _pow(self, name: str, node: Binary) -> None:
         base, ex = node.left, node.right
@@ -384,7 +417,33 @@ class _VecEmitter:
         self.lines.append(f"    for (int j = 1; j < MUSR_PT; ++j) {name}[j] = musr_pow_anchored({self.ref(base, 'j')}, an_, ok); }}")
 
 
-def lower(ast: Node) -> Lowered:
+ROT_TABLE = 15  # bins per run a rotation table covers (MUSR_PT <= ROT_TABLE + 1)
+
+
+def _affine_slope(arg: Node, uniform) -> Optional[Node]:
+    """W when ``arg`` is ``W*t``, ``t*W``, ``W*t +/- Phi`` or ``Phi + W*t`` with W
+    and Phi bin-uniform, else None."""
+    def slope(x):
+        if isinstance(x, Binary) and x.op == "*":
+            if isinstance(x.right, TimeVar) and uniform(x.left):
+                return x.left
+            if isinstance(x.left, TimeVar) and uniform(x.right):
+                return x.right
+        return None
+
+    w = slope(arg)
+    if w is not None:
+        return w
+    if isinstance(arg, Binary) and arg.op in ("+", "-"):
+        w = slope(arg.left)
+        if w is not None and uniform(arg.right):
+            return w
+        if arg.op == "+" and uniform(arg.left):
+            return slope(arg.right)
+    return None
+
+
+def lower(ast: Node, rotate: bool = True) -> Lowered:
     events: List[StaticEvent] = []
     folded, pyval = _events_and_fold(ast, events)
     prim = _desugar(folded)
@@ -421,6 +480,24 @@ def lower(ast: Node) -> Lowered:
         order.append(prim)
         hoisted[prim] = 0
 
+    # cos/sin of affine arguments get a per-dataset rotation table
+    rotations: Dict[Node, int] = {}
+    slopes: List[Node] = []
+
+    def find_rot(n: Node) -> None:
+        if isinstance(n, Call) and n.name in ("cos", "sin") and not uniform(n):
+            a = n.args[0]
+            w = _affine_slope(a, uniform)
+            if w is not None and a not in rotations:
+                rotations[a] = len(slopes)
+                slopes.append(w)
+        for c in (n.operand,) if isinstance(n, Unary) else (n.left, n.right) \
+                if isinstance(n, Binary) else n.args if isinstance(n, Call) else ():
+            find_rot(c)
+
+    if rotate and per_bin:
+        find_rot(prim)
+
     # 2) uniform prologue: slot loads through the per-histogram map row
     def uleaf(n: Node) -> Optional[str]:
         if isinstance(n, SlotRef):
@@ -438,6 +515,17 @@ def lower(ast: Node) -> Lowered:
         val = ue.value(n)
         u_lines.extend(ue.lines)
         u_lines.append(f"  U[{i}] = {val};")
+    nu_reg = max(len(order), 1)
+    rot_lines: List[str] = []
+    for r, w in enumerate(slopes):   # rotation table entry j: D_j = W*(j*dt), cos D_j, sin D_j
+        wv = _lit(float(w.value)) if isinstance(w, Num) else f"U[{hoisted[w]}]"
+        base = nu_reg + 3 * (ROT_TABLE + 1) * r
+        rot_lines.append(f"  {{ const double d_ = __dmul_rn({wv}, __dmul_rn((double)j, dt));")
+        rot_lines.append("    double s_, c_; bool ok_ = true;")
+        rot_lines.append("    musr_sincos_fast(d_, &s_, &c_, ok_);")
+        rot_lines.append("    if (!ok_) { c_ = musr_cos(d_); s_ = musr_sin(d_); }")
+        rot_lines.append(f"    U[{base} + 3 * j] = d_; U[{base} + 3 * j + 1] = c_; "
+                         f"U[{base} + 3 * j + 2] = s_; }}")
 
     # 3) per-bin body: a branch-free fast variant that clears `ok` when an
     #    argument leaves the fast domain, and the exact variant the kernel
@@ -458,14 +546,28 @@ def lower(ast: Node) -> Lowered:
         bodies[fast] = (be.lines, result)
 
     nu = len(order)
+    n_row = nu_reg + 3 * (ROT_TABLE + 1) * len(slopes)
     src: List[str] = []
-    src.append(f"#define MUSR_NU {max(nu, 1)}")
+    src.append(f"#define MUSR_NU {n_row}")
+    src.append(f"#define MUSR_NU_REG {nu_reg}")
+    src.append(f"#define MUSR_NROT {len(slopes)}")
+    if slopes:
+        src.append(f"#if MUSR_PT > {ROT_TABLE + 1}")
+        src.append("#error rotation tables cover at most 16 bins per run")
+        src.append("#endif")
     src.append("__device__ __forceinline__ void musr_uniform(const double* __restrict__ P, "
-               "const int* __restrict__ M, const double* __restrict__ F, double* __restrict__ U) {")
+               "const int* __restrict__ M, const double* __restrict__ F, "
+               "double* __restrict__ U) {")
     src.append("  (void)P; (void)M; (void)F;")
     src.extend(u_lines)
     if nu == 0:
         src.append("  U[0] = 0.0;")
+    src.append("}")
+    # rotation-table entry j (1 <= j < MUSR_PT) of a row whose uniform part U is set
+    src.append("__device__ __forceinline__ void musr_rot_entry(double* __restrict__ U, "
+               "const double dt, const int j) {")
+    src.append("  (void)U; (void)dt; (void)j;")
+    src.extend(rot_lines)
     src.append("}")
     src.append("__device__ __forceinline__ double musr_theory(const double t, "
                "const double* __restrict__ U, bool& ok) {")
@@ -475,12 +577,13 @@ def lower(ast: Node) -> Lowered:
     src.append("}")
     # vectorised per-thread body (anchored transcendentals)
     ve = _VecEmitter(lambda n: _lit(float(n.value)) if isinstance(n, Num) else f"U[{hoisted[n]}]",
-                     uniform)
+                     uniform, rotations if rotate else None)
     if per_bin:
         vres = ve.vec(prim) if not isinstance(prim, TimeVar) else None
     src.append("__device__ __forceinline__ void musr_theory_vec(const double (&t)[MUSR_PT], "
-               "const double* __restrict__ U, double (&A)[MUSR_PT], bool& ok) {")
-    src.append("  (void)t; (void)U; (void)ok;")
+               "const double* __restrict__ U, const double* __restrict__ R, "
+               "double (&A)[MUSR_PT], bool& ok) {")
+    src.append("  (void)t; (void)U; (void)R; (void)ok;")
     if not per_bin:
         val = _lit(float(prim.value)) if isinstance(prim, Num) else f"U[{hoisted[prim]}]"
         src.append("  #pragma unroll")
@@ -504,7 +607,9 @@ def lower(ast: Node) -> Lowered:
     f_slots = [e.slot for e in events if e.kind == "f"]
     return Lowered(
         source="\n".join(src) + "\n",
-        n_uniform=max(nu, 1),
+        n_uniform=n_row,
+        n_uniform_reg=nu_reg,
+        n_rotations=len(slopes),
         uniform_exprs=[_readable(n) for n in order],
         events=events,
         max_p_slot=max(p_slots, default=-1),

@@ -409,7 +409,7 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
   void* params[] = {&a};
   with_table = with_table && c->n_local > kMaxStaged;
   if (with_table)
-    CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1,
+    CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 3) / 4), 1, 1, 128, 1,
                                  1, 0, (CUstream)c->stream, params, nullptr));
   CU_TRY(c, g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, 32 * (c->cwarps + 1), 1, 1,
                                (unsigned)c->dyn_smem[kind], (CUstream)c->stream, params, nullptr));
@@ -496,7 +496,7 @@ int build_graphs(musr_ctx* c) {
     CUresult lr = CUDA_SUCCESS;
     if (c->n_tiles > 0) {
       if (c->n_local > kMaxStaged)
-        lr = g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 127) / 128), 1, 1, 128, 1,
+        lr = g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 3) / 4), 1, 1, 128, 1,
                                 1, 0, (CUstream)c->stream, params, nullptr);
       cudaEventRecordWithFlags(c->kev[kind][0], c->stream, cudaEventRecordExternal);
       if (lr == CUDA_SUCCESS)
@@ -1133,8 +1133,8 @@ int musr_eval_batch(musr_ctx* c, int kind, const double* p, int n_points, int n_
       a.epoch = 0;
       void* params[] = {&a};
       const unsigned rows = (unsigned)(K * c->n_local);
-      CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (rows + 127) / 128, 1, 1, 128, 1, 1, 0,
-                                   (CUstream)c->stream, params, nullptr));
+      CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (rows + 3) / 4, 1, 1, 128, 1, 1, 0,
+                                   (CUstream)c->stream, params, nullptr));  // a warp per row
       CU_TRY(c, g_drv.LaunchKernel(c->fn_batch[kind][c->fmt], c->grid_batch[kind], 1, 1,
                                    32 * (c->cwarps + 1), 1, 1, (unsigned)c->dyn_smem_batch[kind],
                                    (CUstream)c->stream, params, nullptr));

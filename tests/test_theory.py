@@ -108,8 +108,13 @@ def test_round_trip_property(ref):
 
 def test_lowering_structure():
     low = codegen.lower(parse(K_EQ6).ast)
-    assert low.n_uniform == 4              # A0, sigma, 2*pi*K*B, phase
-    assert "musr_exp_fast" in low.source and "musr_cos_fast" in low.source
+    assert low.n_uniform_reg == 4          # A0, sigma, 2*pi*K*B, phase
+    assert low.n_rotations == 1            # tf: cos of an affine argument is rotated
+    assert low.n_uniform == 4 + 3 * (codegen.ROT_TABLE + 1)
+    assert "musr_exp_fast" in low.source and "musr_sincos_fast" in low.source
+    assert "musr_cos_fast" in low.source   # the scalar fast body keeps the direct form
+    plain = codegen.lower(parse(K_EQ6).ast, rotate=False)
+    assert plain.n_rotations == 0 and plain.n_uniform == 4
     assert "musr_theory_exact" in low.source
     # the per-bin body must not touch P/M/F (all slots hoisted)
     body = low.source.split("double musr_theory(")[1].split("}")[0]
