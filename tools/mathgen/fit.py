@@ -49,7 +49,7 @@ def log_table():
         L = -mp.log(mp.mpf(invc))
         h = float(L)
         out.append((invc, h, float(L - mp.mpf(h))))
-    print("MUSR_COEF musr_log_t[128 * 4] = {  // invc, logc_hi, logc_lo, 0")
+    print("... musr_log_t[128 * 4] = {  // invc, logc_hi, logc_lo, 0  (see musr_math.cuh)")
     for invc, h, l in out:
         print(f"    {invc.hex()}, {h.hex()}, {l.hex()}, 0.0,")
     print("};")
