@@ -273,12 +273,12 @@ def main():
     fp64_peak_tflops = _lib.fp64_peak_tflops(local)                # measured DFMA probe
     fp64_instr_peak = fp64_peak_tflops / 2.0                       # T FP64 instr/s (DFMA = 2 flop)
     fp64_alg = ALG_FP64_PER_BIN[args.workload][args.objective] * local_bins / kernel_s / 1e12
-    traffic = None
+    traffic, prof = None, None
     if TRAFFIC_FILE.exists():
         tr = json.loads(TRAFFIC_FILE.read_text())
-        key = f"{args.workload}/{args.objective}"
-        if key in tr:
-            traffic = tr[key]["dram_bytes_per_launch"]
+        prof = tr.get(f"{args.workload}/{args.objective}")
+        if prof is not None and world == 1:
+            traffic = prof["dram_bytes_per_launch"]
     roofline = {
         "bound": "hbm", "achieved": alg_bytes / kernel_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
         "frac": alg_bytes / kernel_s / 1e9 / hbm_peak, "traffic": traffic,
@@ -291,6 +291,15 @@ def main():
                  "alg_instr_per_bin": ALG_FP64_PER_BIN[args.workload][args.objective],
                  "peak_source": f"measured DFMA probe ({fp64_peak_tflops:.1f} TFLOP/s)"},
     }
+    if prof is not None:
+        # what the kernel actually executes (ncu: DADD+DMUL+DFMA thread instructions
+        # per bin, profiles/roofline_traffic.json) at this run's kernel time
+        ex = prof["fp64_thread_inst_per_bin"] * local_bins / kernel_s / 1e12
+        roofline["fp64"]["executed"] = {
+            "achieved": ex, "frac": ex / fp64_instr_peak,
+            "instr_per_bin": prof["fp64_thread_inst_per_bin"],
+            "ncu_fp64_pipe_active_pct": prof["fp64_pipe_active_pct"],
+            "ncu_issue_active_pct": prof["issue_active_pct"], "source": prof["source"]}
 
     # ---- CPU baseline (reference algorithm port, bounded sample) --------------------------
     from oracle import musr_oracle as O
@@ -308,7 +317,11 @@ def main():
         "evals_per_s": evals_per_s, "value_check": value0,
         "e2e": {"value": e2e_value, "unit": "Gbins/s", "evals_per_s": len(e2e_times) / e2e_s,
                 "us_per_call": 1e6 * e2e_s / len(e2e_times),
-                "h2d_bytes_per_step": 8 * len(p), "d2h_bytes_per_step": 16 * len(dss),
+                # p travels in the kernel parameters; results come back as 4
+                # epoch-tagged 8-byte words per dataset (direct path) or 2 fp64
+                # per dataset (sharded graph path)
+                "h2d_bytes_per_step": 8 * len(p),
+                "d2h_bytes_per_step": (32 if world == 1 else 16) * len(dss),
                 "api": "paper_1604_02334_b200.chi2(datasets, expr, p) (reference signature)"},
         "roofline": roofline,
         "cpu_baseline": {"value": cpu_value, "unit": "Gbins/s", "cores": 1, "kind": "port",
