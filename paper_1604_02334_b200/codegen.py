@@ -369,18 +369,20 @@ class _VecEmitter:
 
     def _rotated(self, name: str, fn: str, arg: Node, r: int) -> None:
         a = self.vec(arg)
-        tab = f"(R + MUSR_NU_REG + {3 * (ROT_TABLE + 1) * r})"
+        tab = f"(R + MUSR_NU_REG + {4 * (ROT_TABLE + 1) * r})"
         out = "__fma_rn(-S_, e_, C_)" if fn == "cos" else "__fma_rn(C_, e_, S_)"
         self.lines.append(f"  {{ double s0_, c0_;")
         self.lines.append(f"    musr_sincos_fast({a}[0], &s0_, &c0_, ok);")
         self.lines.append(f"    {name}[0] = {'c0_' if fn == 'cos' else 's0_'};")
         self.lines.append(f"    #pragma unroll")
         self.lines.append(f"    for (int j = 1; j < MUSR_PT; ++j) {{")
-        self.lines.append(f"      const double* tb_ = {tab} + 3 * j;")
-        self.lines.append(f"      const double e_ = __dsub_rn(__dsub_rn({a}[j], {a}[0]), tb_[0]);")
+        self.lines.append(f"      const double* tb_ = {tab} + 4 * j;  // (D_j, cos D_j | sin D_j, -)")
+        self.lines.append(f"      const double2 dc_ = *reinterpret_cast<const double2*>(tb_);")
+        self.lines.append(f"      const double sj_ = tb_[2];")
+        self.lines.append(f"      const double e_ = __dsub_rn(__dsub_rn({a}[j], {a}[0]), dc_.x);")
         self.lines.append(f"      ok = ok && musr_abs_below(e_, 0x3e000000);  // |e| < 2^-31")
-        self.lines.append(f"      const double C_ = __fma_rn(c0_, tb_[1], -__dmul_rn(s0_, tb_[2]));")
-        self.lines.append(f"      const double S_ = __fma_rn(s0_, tb_[1], __dmul_rn(c0_, tb_[2]));")
+        self.lines.append(f"      const double C_ = __fma_rn(c0_, dc_.y, -__dmul_rn(s0_, sj_));")
+        self.lines.append(f"      const double S_ = __fma_rn(s0_, dc_.y, __dmul_rn(c0_, sj_));")
         self.lines.append(f"      {name}[j] = {out};")
         self.lines.append(f"    }} }}")
 
@@ -519,13 +521,13 @@ def lower(ast: Node, rotate: bool = True) -> Lowered:
     rot_lines: List[str] = []
     for r, w in enumerate(slopes):   # rotation table entry j: D_j = W*(j*dt), cos D_j, sin D_j
         wv = _lit(float(w.value)) if isinstance(w, Num) else f"U[{hoisted[w]}]"
-        base = nu_reg + 3 * (ROT_TABLE + 1) * r
+        base = nu_reg + 4 * (ROT_TABLE + 1) * r
         rot_lines.append(f"  {{ const double d_ = __dmul_rn({wv}, __dmul_rn((double)j, dt));")
         rot_lines.append("    double s_, c_; bool ok_ = true;")
         rot_lines.append("    musr_sincos_fast(d_, &s_, &c_, ok_);")
         rot_lines.append("    if (!ok_) { c_ = musr_cos(d_); s_ = musr_sin(d_); }")
-        rot_lines.append(f"    U[{base} + 3 * j] = d_; U[{base} + 3 * j + 1] = c_; "
-                         f"U[{base} + 3 * j + 2] = s_; }}")
+        rot_lines.append(f"    U[{base} + 4 * j] = d_; U[{base} + 4 * j + 1] = c_; "
+                         f"U[{base} + 4 * j + 2] = s_; U[{base} + 4 * j + 3] = 0.0; }}")
 
     # 3) per-bin body: a branch-free fast variant that clears `ok` when an
     #    argument leaves the fast domain, and the exact variant the kernel
@@ -546,7 +548,11 @@ def lower(ast: Node, rotate: bool = True) -> Lowered:
         bodies[fast] = (be.lines, result)
 
     nu = len(order)
-    n_row = nu_reg + 3 * (ROT_TABLE + 1) * len(slopes)
+    # rotation entries are 32-byte aligned (one 16-byte and one 8-byte load):
+    # pad the register part to an even count, and the row (+ N0, Nbkg) stays even
+    if slopes and nu_reg % 2:
+        nu_reg += 1
+    n_row = nu_reg + 4 * (ROT_TABLE + 1) * len(slopes)
     src: List[str] = []
     src.append(f"#define MUSR_NU {n_row}")
     src.append(f"#define MUSR_NU_REG {nu_reg}")

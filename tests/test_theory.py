@@ -110,7 +110,7 @@ def test_lowering_structure():
     low = codegen.lower(parse(K_EQ6).ast)
     assert low.n_uniform_reg == 4          # A0, sigma, 2*pi*K*B, phase
     assert low.n_rotations == 1            # tf: cos of an affine argument is rotated
-    assert low.n_uniform == 4 + 3 * (codegen.ROT_TABLE + 1)
+    assert low.n_uniform == 4 + 4 * (codegen.ROT_TABLE + 1)
     assert "musr_exp_fast" in low.source and "musr_sincos_fast" in low.source
     assert "musr_cos_fast" in low.source   # the scalar fast body keeps the direct form
     plain = codegen.lower(parse(K_EQ6).ast, rotate=False)
