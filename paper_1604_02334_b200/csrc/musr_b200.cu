@@ -448,16 +448,19 @@ int plan_launch(musr_ctx* c) {
     if (kind == 0 && c->fmt == 1) smem_b += (size_t)c->table_size * 16;
     smem_b += (size_t)stages * MUSR_KMAX * c->cwarps * 33 * sizeof(double);  // [S][KMAX][TN_K * 33]
     c->dyn_smem_batch[kind] = smem_b;
+    c->grid_batch[kind] = 0;  // 0: the batched kernel does not fit (musr_eval_batch then
+                              //    evaluates the points one launch at a time)
     CUfunction fb = c->fn_batch[kind][c->fmt];
-    CU_TRY(c, g_drv.FuncSetAttribute(fb, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                                     (int)smem_b));
-    CU_TRY(c, g_drv.FuncSetAttribute(fb, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100));
-    int occ_b = 0;
-    CU_TRY(c, g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, fb, 32 * (c->cwarps + 1),
-                                                               smem_b));
-    if (occ_b < 1) return set_err(c, MUSR_ERR_CUDA, "batched kernel does not fit on an SM");
-    c->grid_batch[kind] =
-        (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, (int64_t)c->sms * occ_b));
+    if (g_drv.FuncSetAttribute(fb, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem_b) ==
+        CUDA_SUCCESS) {
+      CU_TRY(c, g_drv.FuncSetAttribute(fb, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100));
+      int occ_b = 0;
+      CU_TRY(c, g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, fb, 32 * (c->cwarps + 1),
+                                                                 smem_b));
+      if (occ_b >= 1)
+        c->grid_batch[kind] =
+            (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, (int64_t)c->sms * occ_b));
+    }
   }
   if (std::getenv("MUSR_TRACE") && !c->trace) {
     CUDA_TRY(c, cudaMalloc(&c->trace, (size_t)c->sms * 8 * 4 * sizeof(unsigned long long)));
@@ -1116,6 +1119,16 @@ int musr_eval_batch(musr_ctx* c, int kind, const double* p, int n_points, int n_
   if (n_points && n_p && !p) return set_err(c, MUSR_ERR_ARG, "p is NULL");
   CUDA_TRY(c, cudaSetDevice(c->device));
   const int G = c->n_global, cap = c->p_capacity;
+  if (c->n_tiles > 0 && c->grid_batch[kind] == 0) {  // batched kernel does not fit: point by point
+    for (int k = 0; k < n_points; ++k) {
+      const int rc = musr_eval(c, kind, p + (size_t)k * n_p, n_p,
+                               per_dataset ? per_dataset + (size_t)k * G : nullptr,
+                               first_bad_bin ? first_bad_bin + (size_t)k * G : nullptr,
+                               totals ? totals + k : nullptr);
+      if (rc != MUSR_OK) return rc;
+    }
+    return MUSR_OK;
+  }
   for (int base = 0; base < n_points; base += MUSR_KMAX) {
     const int K = std::min(MUSR_KMAX, n_points - base);
     std::memset(c->h_p_batch, 0, (size_t)K * cap * 8);
