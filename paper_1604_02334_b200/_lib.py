@@ -56,6 +56,16 @@ SIGNATURES = [
     ("musr_debug_trace", C.c_int,
      [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]),
     ("musr_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    # muSR data files (struct pointers as void*; musrio.py retypes them with its Structures)
+    ("musr_file_load", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p), C.c_void_p]),
+    ("musr_file_n_detectors", C.c_int, [C.c_void_p]),
+    ("musr_file_detector", C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    ("musr_file_copy", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p]),
+    ("musr_file_free", None, [C.c_void_p]),
+    ("musr_file_store", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_char_p),
+                                  C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int,
+                                  C.c_void_p]),
 ]
 
 _lib: Optional[C.CDLL] = None
