@@ -298,10 +298,11 @@ class _VecEmitter:
     argument a_j of every bin is computed exactly as the reference does, the
     run's first bin gets one full sincos (c0, s0), and bin j uses the
     per-dataset table (D_j = W*(j*dt), cos D_j, sin D_j) built with the
-    uniform row:  cos(a_j) = C_j - S_j*e_j,  sin(a_j) = S_j + C_j*e_j, with
-    C_j + i S_j = (c0 + i s0)(cos D_j + i sin D_j) and e_j = (a_j - a_0) - D_j
-    (|e_j| ~ ulp(a), so the dropped e_j^2 term is < 2^-62).  Per bin 7 FP64
-    operations instead of a reduction and a degree-8 polynomial; the error
+    uniform row:  cos(a_j) = c0*X_j - s0*Y_j,  sin(a_j) = s0*X_j + c0*Y_j,
+    with X_j = cos D_j - e_j*sin D_j, Y_j = sin D_j + e_j*cos D_j and
+    e_j = (a_j - a_0) - D_j (the rotation of (c0, s0) by D_j + e_j to first
+    order; |e_j| ~ ulp(a), so the dropped e_j^2 term is < 2^-62).  Per bin 6
+    FP64 operations instead of a reduction and a degree-8 polynomial; the error
     stays bounded per bin (every run restarts from an evaluated anchor).
     Any argument outside a fast form's window clears ``ok``.
     """
@@ -369,8 +370,11 @@ class _VecEmitter:
 
     def _rotated(self, name: str, fn: str, arg: Node, r: int) -> None:
         a = self.vec(arg)
-        tab = f"(R + MUSR_NU_REG + {4 * (ROT_TABLE + 1) * r})"
-        out = "__fma_rn(-S_, e_, C_)" if fn == "cos" else "__fma_rn(C_, e_, S_)"
+        tab = f"(R + MUSR_NU_REG + 4 * MUSR_PT * {r})"
+        # cos(a0 + D + e) = c0*X - s0*Y, sin(a0 + D + e) = s0*X + c0*Y with
+        # X = cos D - e*sin D, Y = sin D + e*cos D (first order in e; e^2 < 2^-62)
+        out = ("__fma_rn(c0_, X_, -__dmul_rn(s0_, Y_))" if fn == "cos"
+               else "__fma_rn(s0_, X_, __dmul_rn(c0_, Y_))")
         self.lines.append(f"  {{ double s0_, c0_;")
         self.lines.append(f"    musr_sincos_fast({a}[0], &s0_, &c0_, ok);")
         self.lines.append(f"    {name}[0] = {'c0_' if fn == 'cos' else 's0_'};")
@@ -381,8 +385,8 @@ class _VecEmitter:
         self.lines.append(f"      const double sj_ = tb_[2];")
         self.lines.append(f"      const double e_ = __dsub_rn(__dsub_rn({a}[j], {a}[0]), dc_.x);")
         self.lines.append(f"      ok = ok && musr_abs_below(e_, 0x3e000000);  // |e| < 2^-31")
-        self.lines.append(f"      const double C_ = __fma_rn(c0_, dc_.y, -__dmul_rn(s0_, sj_));")
-        self.lines.append(f"      const double S_ = __fma_rn(s0_, dc_.y, __dmul_rn(c0_, sj_));")
+        self.lines.append(f"      const double X_ = __fma_rn(-sj_, e_, dc_.y);")
+        self.lines.append(f"      const double Y_ = __fma_rn(dc_.y, e_, sj_);")
         self.lines.append(f"      {name}[j] = {out};")
         self.lines.append(f"    }} }}")
 
@@ -521,7 +525,7 @@ def lower(ast: Node, rotate: bool = True) -> Lowered:
     rot_lines: List[str] = []
     for r, w in enumerate(slopes):   # rotation table entry j: D_j = W*(j*dt), cos D_j, sin D_j
         wv = _lit(float(w.value)) if isinstance(w, Num) else f"U[{hoisted[w]}]"
-        base = nu_reg + 4 * (ROT_TABLE + 1) * r
+        base = f"(MUSR_NU_REG + 4 * MUSR_PT * {r})"
         rot_lines.append(f"  {{ const double d_ = __dmul_rn({wv}, __dmul_rn((double)j, dt));")
         rot_lines.append("    double s_, c_; bool ok_ = true;")
         rot_lines.append("    musr_sincos_fast(d_, &s_, &c_, ok_);")
@@ -552,11 +556,13 @@ def lower(ast: Node, rotate: bool = True) -> Lowered:
     # pad the register part to an even count, and the row (+ N0, Nbkg) stays even
     if slopes and nu_reg % 2:
         nu_reg += 1
+    # rotation tables hold MUSR_PT entries (the row length follows the tile
+    # configuration the kernel is compiled for); n_row is the MUSR_PT = 16 maximum
     n_row = nu_reg + 4 * (ROT_TABLE + 1) * len(slopes)
     src: List[str] = []
-    src.append(f"#define MUSR_NU {n_row}")
     src.append(f"#define MUSR_NU_REG {nu_reg}")
     src.append(f"#define MUSR_NROT {len(slopes)}")
+    src.append("#define MUSR_NU (MUSR_NU_REG + 4 * MUSR_PT * MUSR_NROT)")
     if slopes:
         src.append(f"#if MUSR_PT > {ROT_TABLE + 1}")
         src.append("#error rotation tables cover at most 16 bins per run")

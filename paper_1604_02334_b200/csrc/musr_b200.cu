@@ -162,7 +162,9 @@ struct musr_ctx {
   int sms = 0;                  // multiprocessors on the device
   int per_thread = 8;           // MUSR_PT: terms per consumer thread
   int cwarps = 16;              // MUSR_CWARPS: consumer warps per CTA; tile = 32*cwarps*per_thread
-  int stages = 2;               // MUSR_STAGES: TMA pipeline depth
+  int stages = 3;               // MUSR_STAGES: deepest TMA pipeline compiled in
+  int stages_used[2] = {0, 0};  // depth that fits per kind (plan_launch)
+  int stages_batch[2] = {0, 0};
   int min_blocks = 1;           // MUSR_MIN_BLOCKS: register budget target
   double* utab = nullptr;       // uniform table (sized at graph build)
   size_t utab_rows = 0;
@@ -256,6 +258,18 @@ __global__ void musr_l2_flush(double4* buf, size_t n, double v) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     buf[i] = make_double4(v, v, v, v);
+}
+
+// flush_l2 == 2: after the write pass, read the first half of the flush buffer
+// so the L2 holds clean lines only (no write-back of the flush's dirty lines
+// inside the timed kernel).  The values written are >= 0, so the sink store
+// never happens; it only keeps the loads alive.
+__global__ void musr_l2_clean(const double4* buf, size_t n, double* sink) {
+  double acc = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    acc += __ldcg(reinterpret_cast<const double2*>(buf + i)).x;
+  if (acc < 0.0) *sink = acc;
 }
 
 // c32 table: {max(1, sqrt(k)), 1 / that}, both correctly rounded like numpy's
@@ -402,6 +416,7 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
   }
   MusrArgs& a = *ap;
   a.epoch = epoch;
+  a.stages = c->stages_used[kind];
   if (n_p >= 0) {
     a.p_inline = 1;
     if (n_p) std::memcpy(a.pin, pinl, sizeof(double) * (size_t)n_p);
@@ -418,49 +433,64 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
 
 constexpr int kTableMax = 4096;         // c32 format: counts must be integers < this
 
-// Persistent grid and dynamic shared memory per objective kind.
+// Deepest TMA pipeline (<= max_stages) whose shared memory fits one CTA per SM:
+// `stage` bytes per stage plus `extra` (table, staged rows); `per_stage`
+// bytes of extra per stage (batched thread-node blocks).  0 if none fits.
+int fit_stages(CUfunction fn, int threads, size_t stage, size_t per_stage, size_t extra,
+               int max_stages, size_t* smem_out, int* occ_out) {
+  for (int st = max_stages; st >= 1; --st) {
+    const size_t smem = (size_t)st * (stage + per_stage) + extra;
+    if (g_drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) !=
+        CUDA_SUCCESS)
+      continue;
+    int occ = 0;
+    if (g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != CUDA_SUCCESS ||
+        occ < 1)
+      continue;
+    g_drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
+    *smem_out = smem;
+    *occ_out = occ;
+    return st;
+  }
+  return 0;
+}
+
+// Persistent grid, TMA pipeline depth and dynamic shared memory per objective
+// kind.  The kernel is compiled for up to MUSR_STAGES stages and takes the
+// depth that fits at run time (MusrArgs::stages): a large count table or many
+// staged datasets cost a stage instead of failing the launch.
 int plan_launch(musr_ctx* c) {
   const size_t tile = (size_t)32 * c->cwarps * c->per_thread;  // terms per tile
+  const int threads = 32 * (c->cwarps + 1);
   for (int kind = 0; kind < 2; ++kind) {
     // MusrGeom in musr_kernel.cuh: d | env | err | rcp
     size_t stage = tile * (c->fmt ? 4 : 8) + tile * 8;
     if (kind == 0 && c->fmt == 0) stage += 2 * tile * 8;
-    const int stages = (kind == 0 && c->fmt == 0 && tile * 32 > 96 * 1024) ? 1 : c->stages;
-    size_t smem = (size_t)stages * stage;  // mirrors the stage count in musr_kernel.cuh
-    if (kind == 0 && c->fmt == 1) smem += (size_t)c->table_size * 16;
-    if (c->n_local <= kMaxStaged)
-      smem += (size_t)c->n_local * (c->n_uniform + 2) * sizeof(double);
-    c->dyn_smem[kind] = smem;
-    CUfunction fn = c->fn[kind][c->fmt];
-    CU_TRY(c, g_drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                                     (int)smem));
-    CU_TRY(c, g_drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100));
+    // mirrors the single stage of the f64 chi2 kernel in musr_kernel.cuh
+    const int max_st = (kind == 0 && c->fmt == 0 && tile * 32 > 96 * 1024) ? 1 : c->stages;
+    size_t extra = 0;
+    if (kind == 0 && c->fmt == 1) extra += (size_t)c->table_size * 16;
+    size_t extra_rows = 0;
+    if (c->n_local <= kMaxStaged) extra_rows = (size_t)c->n_local * (c->n_uniform + 2) * sizeof(double);
     int occ = 0;
-    CU_TRY(c, g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * (c->cwarps + 1),
-                                                               smem));
-    if (occ < 1) return set_err(c, MUSR_ERR_CUDA, "objective kernel does not fit on an SM");
-    const int64_t cap = (int64_t)c->sms * occ;
-    c->grid[kind] = (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, cap));
+    const int st = fit_stages(c->fn[kind][c->fmt], threads, stage, 0, extra + extra_rows, max_st,
+                              &c->dyn_smem[kind], &occ);
+    if (st < 1) return set_err(c, MUSR_ERR_CUDA, "objective kernel does not fit on an SM");
+    c->stages_used[kind] = st;
+    c->grid[kind] = (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, (int64_t)c->sms * occ));
 
     // batched variant: rows come from the global table; the per-point thread
     // nodes take the place of the staged rows (musr_kernel.cuh: s_tn)
-    size_t smem_b = (size_t)stages * stage;
-    if (kind == 0 && c->fmt == 1) smem_b += (size_t)c->table_size * 16;
-    smem_b += (size_t)stages * MUSR_KMAX * c->cwarps * 33 * sizeof(double);  // [S][KMAX][TN_K * 33]
-    c->dyn_smem_batch[kind] = smem_b;
-    c->grid_batch[kind] = 0;  // 0: the batched kernel does not fit (musr_eval_batch then
-                              //    evaluates the points one launch at a time)
-    CUfunction fb = c->fn_batch[kind][c->fmt];
-    if (g_drv.FuncSetAttribute(fb, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem_b) ==
-        CUDA_SUCCESS) {
-      CU_TRY(c, g_drv.FuncSetAttribute(fb, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100));
-      int occ_b = 0;
-      CU_TRY(c, g_drv.OccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, fb, 32 * (c->cwarps + 1),
-                                                                 smem_b));
-      if (occ_b >= 1)
-        c->grid_batch[kind] =
-            (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, (int64_t)c->sms * occ_b));
-    }
+    const size_t tn_block = (size_t)MUSR_KMAX * c->cwarps * 33 * sizeof(double);  // [KMAX][TN_K * 33]
+    int occ_b = 0;
+    const int st_b = fit_stages(c->fn_batch[kind][c->fmt], threads, stage, tn_block, extra, max_st,
+                                &c->dyn_smem_batch[kind], &occ_b);
+    c->stages_batch[kind] = st_b;
+    // 0: the batched kernel does not fit (musr_eval_batch then evaluates the
+    // points one launch at a time)
+    c->grid_batch[kind] =
+        st_b < 1 ? 0u
+                 : (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, (int64_t)c->sms * occ_b));
   }
   if (std::getenv("MUSR_TRACE") && !c->trace) {
     CUDA_TRY(c, cudaMalloc(&c->trace, (size_t)c->sms * 8 * 4 * sizeof(unsigned long long)));
@@ -495,6 +525,7 @@ int build_graphs(musr_ctx* c) {
     cudaMemcpyAsync(c->P, c->h_p, sizeof(double) * c->p_capacity, cudaMemcpyHostToDevice,
                     c->stream);
     MusrArgs a = make_args(c);
+    a.stages = c->stages_used[kind];
     void* params[] = {&a};
     CUresult lr = CUDA_SUCCESS;
     if (c->n_tiles > 0) {
@@ -554,8 +585,11 @@ int open_common(int device, musr_ctx** out, musr_ctx** made) {
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   if (c->sms < 1) c->sms = 1;
   // tuning overrides (defaults are the measured best on B200)
-  if (const char* v = std::getenv("MUSR_PT")) c->per_thread = std::atoi(v) == 4 ? 4 : 8;
-  if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(4, std::atoi(v)));
+  if (const char* v = std::getenv("MUSR_PT")) {
+    const int pt = std::atoi(v);
+    c->per_thread = (pt == 4 || pt == 16) ? pt : 8;
+  }
+  if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(6, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_MIN_BLOCKS")) c->min_blocks = std::max(1, std::min(4, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_CWARPS")) c->cwarps = std::atoi(v) == 8 ? 8 : 16;
   if (c->cwarps == 16) c->min_blocks = std::min(c->min_blocks, 1);  // 544 threads: one CTA per SM
@@ -739,10 +773,15 @@ int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t*
 int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap) {
   if (!c || !fragment) return set_err(c, MUSR_ERR_ARG, "NULL argument");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  int nu = 0;
-  const char* def = std::strstr(fragment, "#define MUSR_NU ");
-  if (!def || std::sscanf(def + 16, "%d", &nu) != 1 || nu < 1)
-    return set_err(c, MUSR_ERR_ARG, "theory fragment must #define MUSR_NU (>= 1)");
+  // row length MUSR_NU = MUSR_NU_REG + 4 * MUSR_PT * MUSR_NROT (codegen.py)
+  int nu_reg = 0, nrot = -1;
+  const char* def = std::strstr(fragment, "#define MUSR_NU_REG ");
+  const char* rot = std::strstr(fragment, "#define MUSR_NROT ");
+  if (!def || std::sscanf(def + 20, "%d", &nu_reg) != 1 || nu_reg < 1 || !rot ||
+      std::sscanf(rot + 18, "%d", &nrot) != 1 || nrot < 0)
+    return set_err(c, MUSR_ERR_ARG,
+                   "theory fragment must #define MUSR_NU_REG (>= 1) and MUSR_NROT (>= 0)");
+  const int nu = nu_reg + 4 * c->per_thread * nrot;
   std::string cubin;
   if (c->have_data && c->per_thread_data != c->per_thread * 100 + c->cwarps)  // layout <-> tile
     return set_err(c, MUSR_ERR_ARG, "tile size changed after upload");
@@ -1080,8 +1119,10 @@ int musr_debug_trace(musr_ctx* c, int kind, uint64_t* out, int cap, int* n_ctas)
   if (!c->trace) return set_err(c, MUSR_ERR_ARG, "handle not built with MUSR_TRACE=1");
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  // [grid][4] basic stamps, then (if cap allows) [grid][4] prologue / first-tile stamps
   const int n = std::min<int>(cap / 4, (int)c->grid[kind]);
-  CUDA_TRY(c, cudaMemcpy(out, c->trace, (size_t)n * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  const size_t words = (cap >= 8 * (int)c->grid[kind]) ? (size_t)8 * n : (size_t)4 * n;
+  CUDA_TRY(c, cudaMemcpy(out, c->trace, words * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   *n_ctas = n;
   return MUSR_OK;
 }
@@ -1144,6 +1185,7 @@ int musr_eval_batch(musr_ctx* c, int kind, const double* p, int n_points, int n_
       a.p_inline = 0;
       a.n_points = K;
       a.epoch = 0;
+      a.stages = c->stages_batch[kind];
       void* params[] = {&a};
       const unsigned rows = (unsigned)(K * c->n_local);
       CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (rows + 3) / 4, 1, 1, 128, 1, 1, 0,
@@ -1191,10 +1233,16 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
     CUDA_TRY(c, cudaMalloc(&c->flush, c->flush_bytes));
     CUDA_TRY(c, cudaFuncSetAttribute(musr_l2_flush, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared));
+    CUDA_TRY(c, cudaFuncSetAttribute(musr_l2_clean, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
   }
   auto flush = [&](int i) -> cudaError_t {
     musr_l2_flush<<<c->sms * 4, 512, 0, c->stream>>>(static_cast<double4*>(c->flush),
                                                      c->flush_bytes / sizeof(double4), (double)i);
+    if (flush_l2 == 2)
+      musr_l2_clean<<<c->sms * 4, 512, 0, c->stream>>>(static_cast<const double4*>(c->flush),
+                                                       c->flush_bytes / 2 / sizeof(double4),
+                                                       static_cast<double*>(c->flush));
     return cudaGetLastError();
   };
   const bool direct = direct_mode(c);

@@ -63,6 +63,8 @@ struct MusrArgs {
   int p_stride;               // batched: P holds n_points rows of p_stride doubles
   int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
   int h_inline;               // 1: hin/min/fin hold all datasets' metadata
+  int stages;                 // TMA pipeline depth of this launch (<= MUSR_STAGES)
+  int pad_;
   double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)
   // Small-problem metadata inline in the kernel parameters: they arrive with
   // the launch, so the CTA prologue issues no dependent global/constant misses.

@@ -93,6 +93,33 @@ def test_device_cos_sin_absolute_error(mathlib):
         assert np.abs(y - f(x)).max() <= 4e-16, name
 
 
+def test_anchored_exp_within_two_ulp(mathlib):
+    """musr_exp_anchored (runs of consecutive bins, |x - x0| < 2^-10) against numpy exp."""
+    rng = np.random.default_rng(5)
+    n = 400_000
+    x0 = np.concatenate([rng.uniform(-700, 700, n), rng.uniform(-20, 0, n)])
+    x = x0 + rng.uniform(-2.0**-10, 2.0**-10, 2 * n) * rng.choice([1.0, 1e-3, 1e-6], 2 * n)
+    y = mathlib("v_exp_anchored", x, x0)
+    ref = np.exp(x)
+    keep = ~np.isnan(y)
+    assert keep.mean() > 0.99
+    assert np.abs(y[keep].view(np.int64) - ref[keep].view(np.int64)).max() <= 2
+    far = mathlib("v_exp_anchored", np.array([1.0 + 2.0**-9, 0.0]), np.array([1.0, 2.0**-9]))
+    assert np.isnan(far).all()  # outside the window: the kernel recomputes exactly
+
+
+def test_rotated_cos_absolute_error(mathlib):
+    """The tf rotation: cos(a0 + D + e) from (cos a0, sin a0), (cos D, sin D) and e."""
+    rng = np.random.default_rng(6)
+    n = 400_000
+    a0 = np.round(rng.uniform(-500, 500, n) * 2.0**20) / 2.0**20  # a0 + D exact in fp64
+    D = np.round(rng.uniform(0, 0.05, n) * 2.0**40) / 2.0**40
+    e = rng.uniform(-1e-13, 1e-13, n)
+    y = mathlib("v_cos_rotated", a0, D, e)
+    ref = np.cos(a0 + D) - np.sin(a0 + D) * e  # e^2 ~ 1e-26 is far below an ulp
+    assert np.abs(y - ref).max() <= 5e-16
+
+
 def test_markstein_division_is_exact(mathlib):
     rng = np.random.default_rng(2)
     n = 1_000_000

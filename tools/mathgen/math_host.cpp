@@ -24,6 +24,15 @@ void v_pow_anchored(const double* x, const double* x0, const double* b, double* 
     if (!ok) y[i] = NAN;
   }
 }
+// rotated cos of a_j = a0 + D + e (codegen.py _rotated): c0*X - s0*Y
+void v_cos_rotated(const double* a0, const double* D, const double* e, double* y, long n) {
+  for (long i = 0; i < n; ++i) {
+    const double c0 = musr_cos(a0[i]), s0 = musr_sin(a0[i]);
+    const double cd = musr_cos(D[i]), sd = musr_sin(D[i]);
+    const double X = fma(-sd, e[i], cd), Y = fma(cd, e[i], sd);
+    y[i] = fma(c0, X, -(s0 * Y));
+  }
+}
 void v_div_y(const double* a, const double* b, const double* yb, double* q, long n) {
   for (long i = 0; i < n; ++i) q[i] = musr_div_y(a[i], b[i], yb[i]);
 }

@@ -15,8 +15,8 @@ for n in names:
 ref = {}
 for v in variants:
     cfg, _, opts = v.partition(":")
-    pt, st, mb = (cfg.split(",") + ["", "", ""])[:3]
-    for key, val in (("MUSR_PT", pt), ("MUSR_STAGES", st), ("MUSR_MIN_BLOCKS", mb)):
+    pt, st, mb, cw = (cfg.split(",") + ["", "", "", ""])[:4]
+    for key, val in (("MUSR_PT", pt), ("MUSR_STAGES", st), ("MUSR_MIN_BLOCKS", mb), ("MUSR_CWARPS", cw)):
         if val:
             os.environ[key] = val
         else:
@@ -32,8 +32,9 @@ for v in variants:
             key = (n, kind)
             if key not in ref:
                 ref[key] = val
-            s.time_evals(kind, 20, 1, True)
-            ms_k = s.time_evals(kind, 100, 1, True) / 100
+            fl = int(os.environ.get("MUSR_FLUSH", "1"))
+            s.time_evals(kind, 20, 1, fl)
+            ms_k = s.time_evals(kind, 100, 1, fl) / 100
             ms_g = s.time_evals(kind, 400, 0) / 400
             out.append(f"{'chi2' if kind == 0 else 'mlh'} kernel {1e3*ms_k:7.1f}us ({nb/ms_k/1e6:6.1f} Gbins/s) graph {1e3*ms_g:7.1f}us ({nb/ms_g/1e6:6.1f}) same={val == ref[key]}")
         print(f"[{v or 'default'}] {n} tiles={s.n_tiles()} | " + " | ".join(out), flush=True)

@@ -12,7 +12,7 @@ ds = W.synthesize(w)
 s = objective.session_for(ds, w.expr, musr.TAU_MU_US, len(w.params), objective.DeviceBackend())
 for kind in (0, 1):
     (musr.chi2 if kind == 0 else musr.mlh)(ds, w.expr, w.params)
-    ms = s.time_evals(kind, 3, 1, True) / 3
+    ms = s.time_evals(kind, 3, 1, int(os.environ.get("MUSR_FLUSH", "1"))) / 3
     buf = (C.c_uint64 * (4 * 4096))()
     n = C.c_int()
     _lib.check(s._lib.musr_debug_trace(s._handle, kind, buf, len(buf), C.byref(n)), s._handle, "trace")
@@ -27,8 +27,13 @@ for kind in (0, 1):
     print("  tiles/CTA min %d max %d; 10 latest CTAs (exit us, tiles): %s" % (
         tiles.min(), tiles.max(), [(round(ex[i], 1), int(tiles[i])) for i in order[-10:]]))
     print("  10 earliest: %s" % [(round(ex[i], 1), int(tiles[i])) for i in order[:10]])
-    for label, col in (("start", 0), ("after prologue", 1), ("producer exit", 3)):
-        v = rel[:, col]
+    ext = np.array(buf[4 * n.value: 8 * n.value], dtype=np.int64).reshape(-1, 4).astype(float)
+    ext_rel = (ext - t0) / 1e3
+    ext_rel[ext == 0] = np.nan
+    cols = [("start", rel[:, 0]), ("rows done", ext_rel[:, 0]), ("rows barrier", ext_rel[:, 1]),
+            ("after prologue", rel[:, 1]), ("1st data", ext_rel[:, 2]), ("1st tile done", ext_rel[:, 3]),
+            ("producer exit", rel[:, 3])]
+    for label, v in cols:
         v = v[~np.isnan(v)]
         if len(v):
             print(f"  {label:14s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us  (n={len(v)})")
