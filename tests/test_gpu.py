@@ -314,3 +314,42 @@ def test_minimize_batched_simplex_identical_to_unbatched():
     assert np.array_equal(batched.best_parameters.values, single.best_parameters.values)
     assert batched.objective_value == single.objective_value
     assert batched.objective_evaluations == single.objective_evaluations
+
+
+# -- full BASELINE sizes and pipeline-depth invariance -----------------------------------
+
+def test_full_size_c4_sampled_parity():
+    """C4 at its full size (64 x 2^22 bins, one GPU): per-dataset values of a
+    sample of datasets against the oracle (each dataset's sum is independent of
+    the others), and the total equals the left fold of the per-dataset values."""
+    w = workloads.c4()
+    dss = workloads.synthesize(w)
+    for kind in ("chi2", "mlh"):
+        total, per = _gpu(kind, dss, w.expr, w.params)
+        folded = 0.0
+        for v in per:
+            folded = folded + v                                  # musr.py:190-201
+        assert folded == total
+        for j in (0, 21, 42, 63):
+            o, _ = _oracle(kind, [dss[j]], w.expr, w.params)
+            assert rel(per[j], o) <= TOL, (kind, j, per[j], o)
+
+
+def test_pipeline_depth_and_large_table_invariance(monkeypatch):
+    """The TMA pipeline depth is picked at run time (the deepest that fits next
+    to the count table and the staged rows): 1, 2 and 3 stages give identical
+    bits, also with a 4096-entry count table and 64 staged datasets."""
+    rng = np.random.default_rng(9)
+    w = workloads.c4(n_hist=64, nbins=20000)
+    dss = workloads.synthesize(w)
+    dss[5].counts[7] = 4095.0                      # table_size 4096 (64 KB of shared memory)
+    p = w.params.copy()
+    p[4] = 1500.0 + 200.0 * rng.standard_normal()
+    got = {}
+    for st in ("1", "2", "3"):
+        monkeypatch.setenv("MUSR_STAGES", st)
+        objective.clear_cache()
+        got[st] = [_gpu(k, dss, w.expr, p)[0] for k in ("chi2", "mlh")]
+    assert got["1"] == got["2"] == got["3"]
+    for i, kind in enumerate(("chi2", "mlh")):
+        assert rel(got["3"][i], _oracle(kind, dss, w.expr, p)[0]) <= TOL
