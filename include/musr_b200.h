@@ -136,7 +136,9 @@ int musr_eval_batch(musr_ctx* ctx, int kind, const double* p, int n_points, int 
  *   mode 2: `iters` graph replays, each bracketed by events -> *ms = summed
  *           evaluation time, *kernel_ms = summed time of the objective kernel
  *           inside those same replays (event nodes captured in the graph).
- *   flush_l2 (modes 1, 2): 1 = write 512 MiB before each iteration, outside the
+ *   mode 3: no evaluation -- only the L2 flush below, then a stream sync (the
+ *           caller times an end-to-end call right after it).
+ *   flush_l2 (modes 1, 2, 3): 1 = write 512 MiB before each iteration, outside the
  *   timed interval, so inputs never start L2-resident; 2 = that, then read
  *   256 MiB of it back, so the L2 also holds no dirty lines whose write-back
  *   would land inside the timed interval. */

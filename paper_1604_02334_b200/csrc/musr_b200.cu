@@ -1228,7 +1228,7 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
   CUDA_TRY(c, cudaEventCreate(&e0));
   CUDA_TRY(c, cudaEventCreate(&e1));
   double total = 0.0, ktotal = 0.0;
-  if ((mode == 1 || mode == 2) && flush_l2 && !c->flush) {
+  if ((mode == 1 || mode == 2 || mode == 3) && flush_l2 && !c->flush) {
     c->flush_bytes = (size_t)512 << 20;  // > 126 MB L2
     CUDA_TRY(c, cudaMalloc(&c->flush, c->flush_bytes));
     CUDA_TRY(c, cudaFuncSetAttribute(musr_l2_flush, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1246,7 +1246,10 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
     return cudaGetLastError();
   };
   const bool direct = direct_mode(c);
-  if (mode == 2) {  // evaluations, each bracketed by events, L2 flushed (untimed) before each
+  if (mode == 3) {  // L2 flush only (before an end-to-end call timed by the caller)
+    if (flush_l2) CUDA_TRY(c, flush(0));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  } else if (mode == 2) {  // evaluations, each bracketed by events, L2 flushed (untimed) before each
     for (int i = 0; i < iters; ++i) {
       if (flush_l2) CUDA_TRY(c, flush(i));
       CUDA_TRY(c, cudaEventRecord(e0, c->stream));

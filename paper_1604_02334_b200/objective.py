@@ -419,9 +419,10 @@ class Session:
 
     def time_evals(self, kind: int, iters: int, mode: int, flush_l2: int = 0):
         """Device timing (see musr_time_evals): returns ms for modes 0/1 and
-        (eval_ms, kernel_ms) for mode 2.  flush_l2: 0 none, 1 write a 512 MB
-        buffer before every timed launch, 2 that plus a 256 MB read pass (the
-        L2 then holds clean lines only)."""
+        (eval_ms, kernel_ms) for mode 2; mode 3 only flushes (before a call the
+        caller times).  flush_l2: 0 none, 1 write a 512 MB buffer before every
+        timed launch, 2 that plus a 256 MB read pass (the L2 then holds clean
+        lines only)."""
         ms, kms = C.c_double(0.0), C.c_double(0.0)
         _lib.check(self._lib.musr_time_evals(self._handle, kind, iters, mode, int(flush_l2),
                                              C.byref(ms), C.byref(kms)),
