@@ -11,7 +11,12 @@ uniform-table kernel, objective kernel (model + residual + pairwise tree),
   2^20 bins, Gaussian-relaxed TF precession (Eq. 6) with per-detector maps.
 * N > 1 (torchrun, one process per GPU): weak scaling -- every rank owns a
   C2-shaped shard (8 datasets x 2^20 bins), all ranks evaluate ONE joint
-  chi2 over 8N datasets.  `value` is whole-job bins/s.
+  chi2 over 8N datasets.  `value` is whole-job bins/s.  The
+  ranks' per-dataset results meet in a host buffer they all map (each rank's
+  kernel writes its datasets' epoch-tagged results there; no device
+  collective); torch.distributed is only the launch / barrier / max plumbing.
+  MUSR_BENCH_DEVICE=<d> puts every rank on device d (functional check of the
+  N > 1 path on one GPU; gloo plumbing).
 
 `value` (Gbins/s) is device-timed with CUDA events on the library's stream,
 inputs resident in HBM, L2 flushed (untimed) before every timed evaluation
@@ -173,8 +178,10 @@ def metric_name(args):
 def workload_config(args, w, world):
     return {"workload": args.workload, "objective": args.objective,
             "datasets": w.n_hist, "bins_per_dataset": w.nbins,
-            "theory": w.expr.source, "parallelism": f"dp{world} (dataset shards, 1 fp64 allreduce/eval)"
-            if world > 1 else "single GPU", "l2": "flushed before every timed evaluation (untimed)"}
+            "theory": w.expr.source,
+            "parallelism": f"dp{world} (dataset shards; results combined in a host buffer mapped by "
+                           f"all ranks, no device collective)" if world > 1 else "single GPU",
+            "l2": "flushed before every timed evaluation (untimed)"}
 
 
 def main():
@@ -198,12 +205,18 @@ def main():
     from paper_1604_02334_b200 import _lib, objective
 
     dist = None
+    same_device = os.environ.get("MUSR_BENCH_DEVICE")
+    if same_device is not None:
+        local = int(same_device)
     if world > 1:
         import torch
         import torch.distributed as dist  # noqa: F811  (plumbing: rendezvous, barrier, max)
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_device is None:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         backend = pkg.DeviceBackend.from_torch_distributed(local)
     else:
         backend = pkg.DeviceBackend(device=local)
@@ -232,7 +245,8 @@ def main():
     if dist is not None:
         import torch
 
-        t = torch.tensor([ms, kms], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([ms, kms], dtype=torch.float64,
+                         device=f"cuda:{local}" if same_device is None else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kms = t.tolist()
     value = total_bins * args.steps / (ms * 1e-3) / 1e9            # whole job, Gbins/s
@@ -254,7 +268,8 @@ def main():
     if dist is not None:
         import torch
 
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([e2e_s], dtype=torch.float64,
+                         device=f"cuda:{local}" if same_device is None else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = t.item()
     e2e_value = total_bins * len(e2e_times) / e2e_s / 1e9
@@ -318,10 +333,10 @@ def main():
         "e2e": {"value": e2e_value, "unit": "Gbins/s", "evals_per_s": len(e2e_times) / e2e_s,
                 "us_per_call": 1e6 * e2e_s / len(e2e_times),
                 # p travels in the kernel parameters; results come back as 4
-                # epoch-tagged 8-byte words per dataset (direct path) or 2 fp64
-                # per dataset (sharded graph path)
+                # epoch-tagged 8-byte words per dataset (all ranks' datasets
+                # land in the shared host buffer when sharded)
                 "h2d_bytes_per_step": 8 * len(p),
-                "d2h_bytes_per_step": (32 if world == 1 else 16) * len(dss),
+                "d2h_bytes_per_step": 32 * len(dss),
                 "api": f"paper_1604_02334_b200.{args.objective}(datasets, expr, p) (reference signature)"},
         "roofline": roofline,
         "cpu_baseline": {"value": cpu_value, "unit": "Gbins/s", "cores": 1, "kind": "port",

@@ -77,6 +77,22 @@ int musr_nccl_unique_id(const char* nccl_lib, unsigned char out_id[128]);
 int musr_open_sharded(int device, int rank, int world, const char* nccl_lib,
                       const unsigned char unique_id[128], musr_ctx** out);
 
+/* Multi-GPU without a device collective: rank `rank`
+ * of `world` processes on one node, each owning a contiguous shard of the
+ * datasets (musr_upload's out_index gives every local dataset its global
+ * slot).  `buf` is host memory shared by all ranks' processes (e.g. one
+ * /dev/shm mapping, zero-filled, 64-byte aligned, >= 64 * n_global bytes);
+ * the library registers it as mapped memory and every rank's objective kernel
+ * writes its datasets' results there as epoch-tagged 8-byte words, so each
+ * host reads every dataset's result directly -- the per-evaluation exchange
+ * rides on the stage-2 stores, no ncclAllReduce and no device sync.  Double-
+ * buffered by epoch parity.  `epoch_base` must differ between the handles
+ * sharing a buffer (same value on every rank).  At most 64 datasets per rank.
+ * Replaces the reference's single-process dataset loop (musr.py:190-201) for
+ * sharded runs; values are bitwise identical to one GPU. */
+int musr_open_shared(int device, int rank, int world, void* buf, size_t bytes,
+                     unsigned long long epoch_base, musr_ctx** out);
+
 void musr_close(musr_ctx* ctx);
 const char* musr_last_error(const musr_ctx* ctx);
 

@@ -38,6 +38,8 @@ SIGNATURES = [
     ("musr_nccl_unique_id", C.c_int, [C.c_char_p, C.c_char_p]),
     ("musr_open_sharded", C.c_int,
      [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    ("musr_open_shared", C.c_int,
+     [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_uint64, C.POINTER(C.c_void_p)]),
     ("musr_close", None, [C.c_void_p]),
     ("musr_last_error", C.c_char_p, [C.c_void_p]),
     ("musr_set_theory", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_size_t]),

@@ -23,6 +23,8 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <chrono>
+#include <map>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -209,6 +211,14 @@ struct musr_ctx {
   MusrArgs direct_args;         // prebuilt direct-launch arguments (only pin[]/epoch change)
   unsigned long long* ll_host = nullptr;  // mapped LL result words (direct path), 4 per dataset
   unsigned long long* ll_dev = nullptr;
+  // Shared results (musr_open_shared): every rank's kernel writes its datasets'
+  // LL words into one host buffer mapped by all ranks' processes (double-
+  // buffered by epoch parity), so each host reads every dataset's result
+  // without a device collective.
+  unsigned long long* shared_host = nullptr;  // caller-owned, registered mapped
+  unsigned long long* shared_dev = nullptr;
+  size_t shared_bytes = 0;
+  unsigned long long epoch_base = 0;
   unsigned long long epoch = 0;
   bool direct_args_ok = false;
   bool h_inline = false;        // metadata small enough for kernel-parameter space
@@ -344,7 +354,7 @@ void free_data(musr_ctx* c) {
   if (c->h_p_batch) cudaFreeHost(c->h_p_batch);
   if (c->h_out_batch) cudaFreeHost(c->h_out_batch);
   c->h_p_batch = c->h_out_batch = nullptr;
-  if (c->ll_host) cudaFreeHost(c->ll_host);
+  if (c->ll_host && c->ll_host != c->shared_host) cudaFreeHost(c->ll_host);
   c->ll_host = c->ll_dev = nullptr;
   if (c->h_p) cudaFreeHost(c->h_p);
   if (c->h_out) cudaFreeHost(c->h_out);
@@ -416,6 +426,9 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
   }
   MusrArgs& a = *ap;
   a.epoch = epoch;
+  if (c->shared_host)  // double-buffered by epoch parity: a rank running one evaluation
+    a.ll = c->ll_dev + (size_t)(epoch & 1ull) * 4 * c->n_global;  // ahead never overwrites
+
   a.stages = c->stages_used[kind];
   if (n_p >= 0) {
     a.p_inline = 1;
@@ -662,11 +675,56 @@ int musr_open_sharded(int device, int rank, int world, const char* nccl_lib,
   return MUSR_OK;
 }
 
+// Shared result buffers are registered once per process (several handles of
+// one backend share a buffer).
+static std::mutex g_shared_mu;
+static std::map<void*, int> g_shared_refs;
+
+int musr_open_shared(int device, int rank, int world, void* buf, size_t bytes,
+                     unsigned long long epoch_base, musr_ctx** out) {
+  if (world < 1 || rank < 0 || rank >= world)
+    return set_err(nullptr, MUSR_ERR_ARG, fmt("bad rank %d / world %d", rank, world));
+  if (!buf || bytes < 64 || (reinterpret_cast<uintptr_t>(buf) & 63))
+    return set_err(nullptr, MUSR_ERR_ARG, "shared result buffer must be 64-byte aligned, >= 64 B");
+  musr_ctx* c = nullptr;
+  int rc = open_common(device, out, &c);
+  if (rc != MUSR_OK) return rc;
+  {
+    std::lock_guard<std::mutex> lk(g_shared_mu);
+    if (g_shared_refs[buf]++ == 0) {
+      const cudaError_t ce = cudaHostRegister(buf, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+      if (ce != cudaSuccess) {
+        g_shared_refs.erase(buf);
+        cudaStreamDestroy(c->stream);
+        delete c;
+        return set_err(nullptr, MUSR_ERR_CUDA, fmt("cudaHostRegister: %s", cudaGetErrorString(ce)));
+      }
+    }
+  }
+  void* dev = nullptr;
+  CUDA_TRY(c, cudaHostGetDevicePointer(&dev, buf, 0));
+  c->shared_host = static_cast<unsigned long long*>(buf);
+  c->shared_dev = static_cast<unsigned long long*>(dev);
+  c->shared_bytes = bytes;
+  c->epoch_base = epoch_base;
+  c->rank = rank;
+  c->world = world;
+  *out = c;
+  return MUSR_OK;
+}
+
 void musr_close(musr_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_data(c);
+  if (c->shared_host) {
+    std::lock_guard<std::mutex> lk(g_shared_mu);
+    if (--g_shared_refs[c->shared_host] == 0) {
+      g_shared_refs.erase(c->shared_host);
+      cudaHostUnregister(c->shared_host);
+    }
+  }
   if (c->mod) g_drv.ModuleUnload(c->mod);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   if (c->flush) cudaFree(c->flush);
@@ -818,6 +876,14 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   if (!c) return set_err(c, MUSR_ERR_ARG, "NULL handle");
   if (n_global < 1 || n_local < 0 || n_local > n_global)
     return set_err(c, MUSR_ERR_ARG, fmt("bad dataset counts %d/%d", n_local, n_global));
+  if (c->shared_host) {
+    if (n_local > kMaxStaged)
+      return set_err(c, MUSR_ERR_ARG, fmt("shared results take at most %d datasets per rank (%d); "
+                                          "use the NCCL-sharded handle", kMaxStaged, n_local));
+    if ((size_t)2 * 4 * 8 * n_global > c->shared_bytes)
+      return set_err(c, MUSR_ERR_ARG, fmt("shared result buffer of %zu bytes is too small for "
+                                          "%d datasets", c->shared_bytes, n_global));
+  }
   if (map_stride < 1 || f_stride < 1 || p_capacity < 1)
     return set_err(c, MUSR_ERR_ARG, "strides and p_capacity must be >= 1");
   CUDA_TRY(c, cudaSetDevice(c->device));
@@ -934,9 +1000,10 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
       cudaHostAlloc((void**)&c->h_out, (size_t)2 * n_global * 8, cudaHostAllocMapped) !=
           cudaSuccess ||
       cudaHostGetDevicePointer((void**)&c->h_out_dev, c->h_out, 0) != cudaSuccess ||
-      cudaHostAlloc((void**)&c->ll_host, (size_t)4 * n_global * 8, cudaHostAllocMapped) !=
-          cudaSuccess ||
-      cudaHostGetDevicePointer((void**)&c->ll_dev, c->ll_host, 0) != cudaSuccess ||
+      (!c->shared_host &&
+       (cudaHostAlloc((void**)&c->ll_host, (size_t)4 * n_global * 8, cudaHostAllocMapped) !=
+            cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&c->ll_dev, c->ll_host, 0) != cudaSuccess)) ||
       cudaHostAlloc((void**)&c->h_p_batch, (size_t)MUSR_KMAX * p_capacity * 8,
                     cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc((void**)&c->h_out_batch, (size_t)MUSR_KMAX * 2 * n_global * 8,
@@ -1001,9 +1068,15 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   }
   CUDA_TRY(c, cudaMemset(c->count, 0, (size_t)n_local * 4));
   CUDA_TRY(c, cudaMemset(c->sched, 0, 2 * sizeof(unsigned)));
-  std::memset(c->ll_host, 0, (size_t)4 * n_global * 8);
+  if (c->shared_host) {  // epochs unique per session: stale words never match, no clearing
+    c->ll_host = c->shared_host;
+    c->ll_dev = c->shared_dev;
+    c->epoch = c->epoch_base;
+  } else {
+    std::memset(c->ll_host, 0, (size_t)4 * n_global * 8);
+    c->epoch = 0;
+  }
   std::memset(c->h_out, 0, (size_t)2 * n_global * 8);
-  c->epoch = 0;
   CUDA_TRY(c, cudaMemset(c->bad, 0xff, (size_t)MUSR_KMAX * n_local * 8));
   CUDA_TRY(c, cudaMemset(c->out_send, 0, (size_t)MUSR_KMAX * 2 * n_global * 8));
   CUDA_TRY(c, cudaMemset(c->out_recv, 0, (size_t)MUSR_KMAX * 2 * n_global * 8));
@@ -1060,12 +1133,13 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
   }
   c->last_p.assign(p, p + n_p);
   static const bool no_flag = std::getenv("MUSR_NO_FLAG") != nullptr;
-  const bool flagged = direct_mode(c) && c->n_tiles > 0 && !no_flag;
+  const bool flagged = direct_mode(c) && (c->n_tiles > 0 || c->shared_host) && !no_flag;
   if (flagged) {
     c->epoch += 1;
     if ((uint32_t)c->epoch == 0) c->epoch += 1;  // 0 marks "never written"
   }
-  int rc = launch_eval(c, kind, flagged ? c->epoch : 0);
+  int rc = (c->n_tiles > 0 || !c->shared_host) ? launch_eval(c, kind, flagged ? c->epoch : 0)
+                                                : MUSR_OK;  // a rank without datasets only reads
   if (rc != MUSR_OK) return rc;
   const int G = c->n_global;
   if (flagged) {
@@ -1075,22 +1149,30 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
     // has retired.  Bounded: after ~20 ms a stream sync (which reports
     // errors), after which every word is current.
     const uint32_t e32 = (uint32_t)c->epoch;
-    volatile unsigned long long* ll = c->ll_host;
+    // shared results: every rank's datasets, in this epoch's half of the buffer
+    const bool shared = c->shared_host != nullptr;
+    const int n_read = shared ? G : c->n_local;
+    auto out_of = [&](int j) { return shared ? j : c->hist_host[j].out_index; };
+    volatile unsigned long long* ll = c->ll_host + (shared ? (size_t)(c->epoch & 1ull) * 4 * G : 0);
     int i = 0, w = 0;
-    for (long spin = 0; i < c->n_local && spin <= (1L << 22); ++spin) {
-      const int o = c->hist_host[i].out_index;
+    // other ranks may still be uploading or evaluating: a longer bound when shared
+    const auto t_start = std::chrono::steady_clock::now();
+    const auto bound = shared ? std::chrono::seconds(120) : std::chrono::seconds(1);
+    for (long spin = 0; i < n_read; ++spin) {
+      const int o = out_of(i);
       while (w < 4 && (uint32_t)ll[4 * o + w] == e32) ++w;
       if (w == 4) { ++i; w = 0; }
+      if ((spin & 4095) == 4095 && std::chrono::steady_clock::now() - t_start > bound) break;
     }
-    if (i < c->n_local) {
+    if (i < n_read) {
       CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-      for (int j = 0; j < c->n_local; ++j)
+      for (int j = 0; j < n_read; ++j)
         for (int q = 0; q < 4; ++q)
-          if ((uint32_t)ll[4 * c->hist_host[j].out_index + q] != e32)
+          if ((uint32_t)ll[4 * out_of(j) + q] != e32)
             return set_err(c, MUSR_ERR_CUDA, "evaluation finished without its results");
     }
-    for (int j = 0; j < c->n_local; ++j) {
-      const int o = c->hist_host[j].out_index;
+    for (int j = 0; j < n_read; ++j) {
+      const int o = out_of(j);
       const unsigned long long* x = (const unsigned long long*)ll + 4 * o;
       const unsigned long long s = ((x[0] >> 32) << 32) | (x[1] >> 32);
       const unsigned long long b = ((x[2] >> 32) << 32) | (x[3] >> 32);
@@ -1160,7 +1242,9 @@ int musr_eval_batch(musr_ctx* c, int kind, const double* p, int n_points, int n_
   if (n_points && n_p && !p) return set_err(c, MUSR_ERR_ARG, "p is NULL");
   CUDA_TRY(c, cudaSetDevice(c->device));
   const int G = c->n_global, cap = c->p_capacity;
-  if (c->n_tiles > 0 && c->grid_batch[kind] == 0) {  // batched kernel does not fit: point by point
+  // point by point when the batched kernel does not fit, and with shared results
+  // (each point's results come back through the ranks' shared LL words)
+  if ((c->n_tiles > 0 && c->grid_batch[kind] == 0) || c->shared_host) {
     for (int k = 0; k < n_points; ++k) {
       const int rc = musr_eval(c, kind, p + (size_t)k * n_p, n_p,
                                per_dataset ? per_dataset + (size_t)k * G : nullptr,

@@ -71,10 +71,14 @@ class DeviceBackend:
     """Execution backend for the GPU objective (the DKS device selection).
 
     ``world == 1``: one GPU, no collective.  ``world > 1``: this process is
-    rank ``rank``; datasets are split into contiguous, bin-balanced shards and
-    the per-dataset results are combined by one fp64 ncclAllReduce per
-    evaluation inside the CUDA graph.  Every rank must call the objective with
-    the same datasets and p (SPMD), like the reference's single caller.
+    rank ``rank``; datasets are split into contiguous, bin-balanced shards.
+    The per-dataset results are combined either through ``shared_results``
+    -- a host buffer mapped by every rank's process, into which each rank's
+    kernel writes its datasets' epoch-tagged results (musr_open_shared; the
+    default of ``from_torch_distributed``) -- or by one fp64 ncclAllReduce per
+    evaluation inside a CUDA graph (``nccl_id``).  Every rank must call the
+    objective with the same datasets and p (SPMD), like the reference's single
+    caller.
     """
 
     device: int = 0
@@ -83,6 +87,8 @@ class DeviceBackend:
     nccl_id: Optional[bytes] = field(default=None, repr=False)
     worker_count: int = 1          # accepted for signature compatibility
     collective: bool = False       # force the NCCL path even for world == 1 (tests)
+    # (address, bytes) of the ranks' shared result buffer (shared_result_buffer)
+    shared_results: Optional[Tuple[int, int]] = field(default=None, repr=False)
 
     @property
     def kind(self) -> str:
@@ -90,9 +96,12 @@ class DeviceBackend:
             f"B200(device={self.device}, rank={self.rank}/{self.world})"
 
     @classmethod
-    def from_torch_distributed(cls, device: Optional[int] = None) -> "DeviceBackend":
+    def from_torch_distributed(cls, device: Optional[int] = None,
+                               combine: str = "host") -> "DeviceBackend":
         """Build a sharded backend from an initialised torch.distributed group
-        (plumbing only: the NCCL unique id is broadcast with it)."""
+        (plumbing only).  ``combine="host"``: the ranks share a result buffer
+        in host memory (one node); ``"nccl"``: an NCCL unique id is broadcast
+        for the in-graph ncclAllReduce."""
         import torch.distributed as dist  # plumbing, not the product
 
         rank, world = dist.get_rank(), dist.get_world_size()
@@ -102,11 +111,47 @@ class DeviceBackend:
             device = int(os.environ.get("LOCAL_RANK", rank))
         if world == 1:
             return cls(device=device)
+        if combine == "host":
+            return cls(device=device, rank=rank, world=world,
+                       shared_results=shared_result_buffer(dist))
         holder = [None]
         if rank == 0:
             holder[0] = new_nccl_id()
         dist.broadcast_object_list(holder, src=0)
         return cls(device=device, rank=rank, world=world, nccl_id=holder[0])
+
+
+# Shared result buffers of this process: address -> (mmap, sessions opened on it)
+_SHARED: Dict[int, list] = {}
+SHARED_RESULT_BYTES = 1 << 22      # 2 slots x 4 words x 8 B x 65536 datasets
+
+
+def shared_result_buffer(dist, nbytes: int = SHARED_RESULT_BYTES) -> Tuple[int, int]:
+    """A zero-filled host buffer mapped by every rank of ``dist``'s group (one
+    node): rank 0 creates a /dev/shm file, every rank maps it, and rank 0
+    removes the name once all have (the mappings stay).  Returns (address,
+    bytes) for DeviceBackend.shared_results."""
+    import mmap
+    import os
+    import uuid
+
+    holder = [f"/dev/shm/musr_b200_{uuid.uuid4().hex}" if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(holder, src=0)
+    path = holder[0]
+    if dist.get_rank() == 0:
+        fd = os.open(path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+        os.ftruncate(fd, nbytes)
+    dist.barrier()
+    if dist.get_rank() != 0:
+        fd = os.open(path, os.O_RDWR)
+    mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+    os.close(fd)
+    dist.barrier()
+    if dist.get_rank() == 0:
+        os.unlink(path)
+    addr = C.addressof(C.c_char.from_buffer(mm))
+    _SHARED[addr] = [mm, 0]
+    return addr, nbytes
 
 
 def new_nccl_id() -> bytes:
@@ -300,7 +345,14 @@ class Session:
         p_capacity = max(1, self.n_p)
 
         handle = C.c_void_p()
-        if be.world == 1 and not be.collective:
+        if be.shared_results is not None:
+            addr, nbytes = be.shared_results
+            entry = _SHARED.setdefault(addr, [None, 0])
+            entry[1] += 1            # sessions are created in the same order on every rank
+            _lib.check(lib.musr_open_shared(be.device, be.rank, be.world, C.c_void_p(addr),
+                                            nbytes, entry[1] << 24, C.byref(handle)),
+                       None, "musr_open_shared")
+        elif be.world == 1 and not be.collective:
             _lib.check(lib.musr_open(be.device, C.byref(handle)), None, "musr_open")
         else:
             if be.nccl_id is None or len(be.nccl_id) != 128:

@@ -353,3 +353,71 @@ def test_pipeline_depth_and_large_table_invariance(monkeypatch):
     assert got["1"] == got["2"] == got["3"]
     for i, kind in enumerate(("chi2", "mlh")):
         assert rel(got["3"][i], _oracle(kind, dss, w.expr, p)[0]) <= TOL
+
+
+# -- multi-rank: shared host results (two ranks on this GPU) -----------------------------
+
+def _shared_rank(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    be = pkg.DeviceBackend(device=0, rank=rank, world=world,
+                           shared_results=objective.shared_result_buffer(dist))
+    w = workloads.c2(n_hist=7, nbins=1 << 16)          # 7 datasets: uneven shards
+    dss = workloads.synthesize(w)
+    rng = np.random.default_rng(3)
+    res = []
+    for _ in range(4):
+        p = w.params * (1.0 + 0.03 * rng.standard_normal(len(w.params)))
+        res.append([pkg.chi2(dss, w.expr, p, be), pkg.mlh(dss, w.expr, p, be)])
+    res.append(list(pkg.chi2_batch(dss, w.expr, np.array([w.params, 1.01 * w.params]), be)))
+    expr = pkg.parse("p[m[0]] * t")                     # MLH error raised on every rank
+    bad = [pkg.MusrDataset(j, np.full(400000 - 1000 * j, 50), 0.001, 11, pkg.TheoryBinding(map=(2,)), 0, 1)
+           for j in range(3)]
+    try:
+        pkg.mlh(bad, expr, np.array([1.0, 0.0, -1.0 / 300.0]), be)
+        res.append("no error")
+    except pkg.MusrError as exc:
+        res.append(str(exc))
+    import pickle
+
+    with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as f:
+        pickle.dump([[float(v) for v in x] if not isinstance(x, str) else x for x in res], f)
+    objective.clear_cache()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shared_host_results_two_ranks_match_one_gpu(tmp_path):
+    """Two ranks (processes) on this GPU, each owning half the datasets, combine
+    their results through the shared host buffer: every rank gets the one-GPU
+    values bit for bit, batched calls and the MLH error included."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_shared_rank, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    w = workloads.c2(n_hist=7, nbins=1 << 16)
+    dss = workloads.synthesize(w)
+    rng = np.random.default_rng(3)
+    want = []
+    for _ in range(4):
+        p = w.params * (1.0 + 0.03 * rng.standard_normal(len(w.params)))
+        want.append([pkg.chi2(dss, w.expr, p), pkg.mlh(dss, w.expr, p)])
+    want.append(list(pkg.chi2_batch(dss, w.expr, np.array([w.params, 1.01 * w.params]))))
+    expr = pkg.parse("p[m[0]] * t")
+    bad = [pkg.MusrDataset(j, np.full(400000 - 1000 * j, 50), 0.001, 11, pkg.TheoryBinding(map=(2,)), 0, 1)
+           for j in range(3)]
+    with pytest.raises(pkg.MusrError) as exc:
+        pkg.mlh(bad, expr, np.array([1.0, 0.0, -1.0 / 300.0]))
+    want.append(str(exc.value))
+    import pickle
+
+    want = [[float(v) for v in x] if not isinstance(x, str) else x for x in want]
+    for r in range(2):
+        with open(tmp_path / f"rank{r}.pkl", "rb") as f:
+            assert pickle.load(f) == want, r
