@@ -85,6 +85,11 @@ class MusrDataset:
     nbkg_slot: int
     fit_range: Optional[tuple] = None
 
+    def __setattr__(self, name, value):
+        # any field assignment invalidates the session cache's O(1) check
+        _obj.DATASET_MUTATIONS[0] += 1
+        object.__setattr__(self, name, value)
+
     def __post_init__(self):
         self.counts = np.asarray(self.counts)
         j = self.detector_index
@@ -157,8 +162,11 @@ class FitResult:
 
 # -- objectives (GPU) ------------------------------------------------------------------
 
+_DEFAULT_BACKEND = DeviceBackend()
+
+
 def _device_backend(backend) -> DeviceBackend:
-    return backend if isinstance(backend, DeviceBackend) else DeviceBackend()
+    return backend if isinstance(backend, DeviceBackend) else _DEFAULT_BACKEND
 
 
 def _evaluate(kind: int, datasets, expr, p, backend, constants) -> float:
