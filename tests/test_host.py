@@ -265,6 +265,44 @@ def test_sharded_combination_is_exact_gloo():
         assert total == single   # bitwise: every slot has exactly one non-zero contributor
 
 
+def _shm_worker(rank, world, port, q):
+    import ctypes
+
+    import torch.distributed as dist
+
+    from paper_1604_02334_b200 import objective
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    addr, nbytes = objective.shared_result_buffer(dist, 1 << 16)
+    words = (ctypes.c_uint64 * (nbytes // 8)).from_address(addr)
+    assert all(w == 0 for w in words[:64])               # zero-filled
+    words[rank] = 1000 + rank                            # each rank writes its slot
+    dist.barrier()
+    leftovers = [f for f in os.listdir("/dev/shm") if f.startswith("musr_b200_")]
+    q.put((rank, [words[r] for r in range(world)], addr % 64, leftovers))
+    dist.destroy_process_group()
+
+
+def test_shared_result_buffer_is_one_mapping_gloo():
+    """The ranks' result buffer (musr_open_shared's host side): one zero-filled
+    mapping seen by every rank, aligned, its /dev/shm name already removed."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_shm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, seen, align, leftovers in res:
+        assert seen == [1000, 1001] and align == 0
+        assert leftovers == []     # rank 0 unlinked the name once every rank had mapped it
+
+
 # -- restated Nelder-Mead (optimize.py:41-146) -------------------------------------
 
 def test_minimize_hooks():
