@@ -702,8 +702,13 @@ int musr_open_shared(int device, int rank, int world, void* buf, size_t bytes,
     }
   }
   void* dev = nullptr;
-  CUDA_TRY(c, cudaHostGetDevicePointer(&dev, buf, 0));
-  c->shared_host = static_cast<unsigned long long*>(buf);
+  const cudaError_t dce = cudaHostGetDevicePointer(&dev, buf, 0);
+  c->shared_host = static_cast<unsigned long long*>(buf);  // (released by musr_close)
+  if (dce != cudaSuccess) {
+    musr_close(c);
+    return set_err(nullptr, MUSR_ERR_CUDA,
+                   fmt("cudaHostGetDevicePointer: %s", cudaGetErrorString(dce)));
+  }
   c->shared_dev = static_cast<unsigned long long*>(dev);
   c->shared_bytes = bytes;
   c->epoch_base = epoch_base;
