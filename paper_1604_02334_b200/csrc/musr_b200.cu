@@ -1138,7 +1138,9 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
   }
   c->last_p.assign(p, p + n_p);
   static const bool no_flag = std::getenv("MUSR_NO_FLAG") != nullptr;
-  const bool flagged = direct_mode(c) && (c->n_tiles > 0 || c->shared_host) && !no_flag;
+  // (shared results exist only as LL words: MUSR_NO_FLAG does not apply there)
+  const bool flagged = direct_mode(c) && (c->n_tiles > 0 || c->shared_host) &&
+                       (!no_flag || c->shared_host);
   if (flagged) {
     c->epoch += 1;
     if ((uint32_t)c->epoch == 0) c->epoch += 1;  // 0 marks "never written"
@@ -1151,8 +1153,9 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
     // Each local dataset's stage-2 writer stores its results as LL words
     // carrying this evaluation's epoch; the host reads them as they land
     // (no completion flag, no device-side fence), typically before the kernel
-    // has retired.  Bounded: after ~20 ms a stream sync (which reports
-    // errors), after which every word is current.
+    // has retired.  Bounded: after 1 s (120 s when other ranks' results are
+    // awaited) a stream sync (which reports errors), after which every word of
+    // this rank is current.
     const uint32_t e32 = (uint32_t)c->epoch;
     // shared results: every rank's datasets, in this epoch's half of the buffer
     const bool shared = c->shared_host != nullptr;
