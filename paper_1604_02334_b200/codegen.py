@@ -416,7 +416,9 @@ class _VecEmitter:
 
     def _anchored_pow(self, name: str, base: Node, b: str) -> None:
         x0 = self.ref(base, "0")
-        self.lines.append(f"  {{ const double p0_ = pow({x0}, {b});")
+        # anchor: exp(b * log x0) in extended precision (musr_pow_fast, <= 2 ulp);
+        # outside its domain `ok` drops and the thread's bins are redone exactly
+        self.lines.append(f"  {{ const double p0_ = MUSR_POW_ANCHOR({x0}, {b}, ok);")
         self.lines.append(f"    const MusrPowAnchor an_ = musr_pow_anchor({x0}, p0_, {b});")
         self.lines.append(f"    {name}[0] = p0_;")
         self.lines.append(f"    #pragma unroll")

@@ -108,6 +108,26 @@ def test_anchored_exp_within_two_ulp(mathlib):
     assert np.isnan(far).all()  # outside the window: the kernel recomputes exactly
 
 
+def test_pow_anchor_within_two_ulp(mathlib):
+    """musr_pow_fast (the anchored pow's anchor: exp(b log x) carried in
+    extended precision) against libm pow; musr_rcp_approx to 1 ulp."""
+    import math
+    rng = np.random.default_rng(7)
+    n = 200_000
+    x = np.exp(rng.uniform(-20, 20, n))
+    b = rng.uniform(-4, 4, n)
+    keep = np.abs(b * np.log(x)) < 700
+    x, b = x[keep], b[keep]
+    y = mathlib("v_pow_fast", x, b)
+    ref = np.array([math.pow(u, v) for u, v in zip(x, b)])
+    assert not np.isnan(y).any()
+    assert np.abs(y.view(np.int64) - ref.view(np.int64)).max() <= 2
+    bad = mathlib("v_pow_fast", np.array([0.0, -1.0, np.inf, 1e300]), np.array([1.5, 1.5, 1.5, 3.0]))
+    assert np.isnan(bad).all()   # outside the fast domain: the kernel recomputes exactly
+    r = mathlib("v_rcp_approx", x)
+    assert np.abs(r.view(np.int64) - (1.0 / x).view(np.int64)).max() <= 1
+
+
 def test_rotated_cos_absolute_error(mathlib):
     """The tf rotation: cos(a0 + D + e) from (cos a0, sin a0), (cos D, sin D) and e."""
     rng = np.random.default_rng(6)
@@ -276,11 +296,12 @@ def _shm_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     addr, nbytes = objective.shared_result_buffer(dist, 1 << 16)
     words = (ctypes.c_uint64 * (nbytes // 8)).from_address(addr)
-    assert all(w == 0 for w in words[:64])               # zero-filled
+    zero = all(w == 0 for w in words[:64])               # zero-filled
+    dist.barrier()
     words[rank] = 1000 + rank                            # each rank writes its slot
     dist.barrier()
     leftovers = [f for f in os.listdir("/dev/shm") if f.startswith("musr_b200_")]
-    q.put((rank, [words[r] for r in range(world)], addr % 64, leftovers))
+    q.put((rank, [words[r] for r in range(world)], addr % 64, leftovers, zero))
     dist.destroy_process_group()
 
 
@@ -298,8 +319,8 @@ def test_shared_result_buffer_is_one_mapping_gloo():
     res = [q.get(timeout=120) for _ in procs]
     for pr in procs:
         pr.join(timeout=60)
-    for rank, seen, align, leftovers in res:
-        assert seen == [1000, 1001] and align == 0
+    for rank, seen, align, leftovers, zero in res:
+        assert zero and seen == [1000, 1001] and align == 0
         assert leftovers == []     # rank 0 unlinked the name once every rank had mapped it
 
 

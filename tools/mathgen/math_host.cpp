@@ -33,6 +33,22 @@ void v_cos_rotated(const double* a0, const double* D, const double* e, double* y
     y[i] = fma(c0, X, -(s0 * Y));
   }
 }
+void v_pow_fast(const double* x, const double* b, double* y, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    y[i] = musr_pow_fast(x[i], b[i], musr_log_t, ok);
+    if (!ok) y[i] = NAN;
+  }
+}
+void v_log_hl(const double* x, double* h, double* l, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    musr_log_hl(x[i], musr_log_t, &h[i], &l[i], ok);
+  }
+}
+void v_rcp_approx(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) y[i] = musr_rcp_approx(x[i]);
+}
 void v_div_y(const double* a, const double* b, const double* yb, double* q, long n) {
   for (long i = 0; i < n; ++i) q[i] = musr_div_y(a[i], b[i], yb[i]);
 }
