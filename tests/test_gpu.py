@@ -421,3 +421,21 @@ def test_shared_host_results_two_ranks_match_one_gpu(tmp_path):
     for r in range(2):
         with open(tmp_path / f"rank{r}.pkl", "rb") as f:
             assert pickle.load(f) == want, r
+
+
+def test_long_parameter_vector_not_inline():
+    """n_p > 64 (here 3 + 3 x 24 = 75): p goes through the device buffer, not the
+    kernel parameters; values and batched values still match the oracle."""
+    w = workloads.c2(n_hist=24, nbins=30000)
+    dss = workloads.synthesize(w)
+    assert len(w.params) > 64
+    rng = np.random.default_rng(8)
+    P = np.array([w.params * (1.0 + 0.02 * rng.standard_normal(len(w.params))) for _ in range(3)])
+    for kind in ("chi2", "mlh"):
+        for p in P:
+            g, gp = _gpu(kind, dss, w.expr, p)
+            o, op = _oracle(kind, dss, w.expr, p)
+            assert rel(g, o) <= TOL and max(rel(a, b) for a, b in zip(gp, op)) <= TOL
+        fnb = pkg.chi2_batch if kind == "chi2" else pkg.mlh_batch
+        fn = pkg.chi2 if kind == "chi2" else pkg.mlh
+        assert list(fnb(dss, w.expr, P)) == [fn(dss, w.expr, p) for p in P]
