@@ -827,7 +827,7 @@ extern "C" {
 int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t* cubin_bytes) {
   if (!fragment) return set_err(nullptr, MUSR_ERR_ARG, "NULL fragment");
   std::string cubin;
-  int rc = jit_compile(nullptr, 8, 2, 1, 16, fragment, log, log_cap, &cubin);
+  int rc = jit_compile(nullptr, 8, 3, 1, 16, fragment, log, log_cap, &cubin);  // the defaults
   if (rc != MUSR_OK) return rc;
   if (cubin_bytes) *cubin_bytes = cubin.size();
   return MUSR_OK;
