@@ -158,6 +158,38 @@ int musr_eval_batch(musr_ctx* ctx, int kind, const double* p, int n_points, int 
  *   timed interval, so inputs never start L2-resident; 2 = that, then read
  *   256 MiB of it back, so the L2 also holds no dirty lines whose write-back
  *   would land inside the timed interval. */
+/* Datasets of the whole (possibly sharded) problem after musr_upload. */
+int musr_n_datasets(const musr_ctx* ctx, int* n_global);
+
+/* Native bounded Nelder-Mead (restates optimize.py:41-146, bitwise-identical
+ * iterates) driving musr_eval / musr_eval_batch directly, so a fit does not
+ * return to the host language between evaluations.  p_full: the full
+ * parameter vector (fixed values); free_idx[n_free]: the optimised slots;
+ * x0: the clamped start in free coordinates and f0 its objective value
+ * (evaluated by the caller, which raises the reference's errors there);
+ * step/lo/hi: per free coordinate; budget: maximum evaluations including the
+ * start.  Returns MUSR_OK with best_x[n_free] etc., or MUSR_NM_RAISED when an
+ * evaluation hit a reference error (an MLH non-positive model): fail_x[n_free]
+ * is that point, for the caller to re-evaluate with the reference semantics.
+ * Replaces the minimize -> nelder_mead loop of musr.py:246-296 /
+ * optimize.py:41-146 for the built-in objectives. */
+#define MUSR_NM_RAISED 100
+int musr_minimize(musr_ctx* ctx, int kind, const double* p_full, int n_p, const int32_t* free_idx,
+                  int n_free, const double* x0, double f0, const double* step, const double* lo,
+                  const double* hi, double tol_f, int64_t budget, int restarts, double* best_x,
+                  double* best_f, int64_t* iterations, int64_t* evaluations, int* converged,
+                  double* fail_x);
+
+/* The same loop over a caller-supplied objective (tests: checks the native
+ * loop against optimize.py without a GPU).  eval(user, xs, k, n, fs) fills
+ * fs[0..k) for the k rows of xs; a nonzero return aborts with that status
+ * (fail_x = the point). */
+typedef int (*musr_nm_eval_fn)(void* user, const double* xs, int k, int n, double* fs);
+int musr_nm_run(int n, const double* x0, double f0, const double* step, const double* lo,
+                const double* hi, double tol_f, int64_t budget, int restarts, musr_nm_eval_fn eval,
+                void* user, double* best_x, double* best_f, int64_t* iterations,
+                int64_t* evaluations, int* converged, double* fail_x);
+
 int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, double* ms,
                     double* kernel_ms);
 

@@ -54,6 +54,13 @@ SIGNATURES = [
      [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
       C.POINTER(C.c_double)]),
     ("musr_tiles", C.c_int, [C.c_void_p, _I64P]),
+    ("musr_n_datasets", C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
+    ("musr_minimize", C.c_int,
+     [C.c_void_p, C.c_int, _DP, C.c_int, _I32P, C.c_int, _DP, C.c_double, _DP, _DP, _DP,
+      C.c_double, C.c_int64, C.c_int, _DP, _DP, _I64P, _I64P, C.POINTER(C.c_int), _DP]),
+    ("musr_nm_run", C.c_int,
+     [C.c_int, _DP, C.c_double, _DP, _DP, _DP, C.c_double, C.c_int64, C.c_int, C.c_void_p,
+      C.c_void_p, _DP, _DP, _I64P, _I64P, C.POINTER(C.c_int), _DP]),
     ("musr_format", C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("musr_debug_trace", C.c_int,
      [C.c_void_p, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]),

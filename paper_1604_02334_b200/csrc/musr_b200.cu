@@ -1224,6 +1224,13 @@ int musr_format(const musr_ctx* c, int* format, int* table_size) {
   return MUSR_OK;
 }
 
+int musr_n_datasets(const musr_ctx* c, int* n_global) {
+  if (!c || !n_global) return MUSR_ERR_ARG;
+  if (!c->have_data) return set_err(const_cast<musr_ctx*>(c), MUSR_ERR_ARG, "no data uploaded");
+  *n_global = c->n_global;
+  return MUSR_OK;
+}
+
 int musr_tiles(const musr_ctx* c, int64_t* n_tiles) {
   if (!c || !n_tiles) return MUSR_ERR_ARG;
   *n_tiles = c->n_tiles;

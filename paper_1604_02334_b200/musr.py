@@ -289,10 +289,52 @@ def minimize(
             P[:, free] = X
             return batch_fn(P)
 
+    if batch_fn is not None and len(datasets) > 0:
+        # Built-in objective: the whole loop runs natively (musr_minimize, the
+        # same iterates bit for bit); only the start is evaluated here, so the
+        # reference's errors are raised exactly where nelder_mead raises them.
+        return _minimize_native(objective, datasets, expr, params, backend, constants, config,
+                                free, full, steps, lo, hi, reduced)
     res = nelder_mead(reduced, params.values[free], steps, lo, hi, config, reduced_batch)
     full[free] = res.x
     return FitResult(params.copy_with(full), res.fun, res.iterations, res.evaluations,
                      res.converged)
+
+
+def _minimize_native(objective, datasets, expr, params, backend, constants, config, free, full,
+                     steps, lo, hi, reduced) -> FitResult:
+    import ctypes as C
+
+    from ._lib import check as _check
+    from .optimize import OptimizeError
+
+    cfg = config or MinimizeConfig()
+    x0 = np.minimum(np.maximum(np.asarray(params.values[free], dtype=np.float64), lo), hi)
+    first = reduced(x0)                    # optimize.py:81-83 (static errors raise here)
+    if not np.isfinite(first):
+        raise OptimizeError(f"objective is not finite at the initial point ({first})")
+    full[free] = x0
+    sess = _obj.session_for(datasets, expr, float(constants.tau_mu), len(full),
+                            _device_backend(backend))
+    n = len(free)
+    kind = KIND_CHI2 if objective == "chi2" else KIND_MLH
+    dp = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+    pf, x0c, st, lo_, hi_ = dp(full), dp(x0), dp(steps), dp(lo), dp(hi)
+    idx = np.ascontiguousarray(free, dtype=np.int32)
+    best, fail = np.zeros(n), np.zeros(n)
+    bf, it, ev, conv = C.c_double(), C.c_int64(), C.c_int64(), C.c_int()
+    P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    rc = sess._lib.musr_minimize(sess._handle, kind, P(pf), len(pf),
+                                 idx.ctypes.data_as(C.POINTER(C.c_int32)), n, P(x0c), first, P(st),
+                                 P(lo_), P(hi_), cfg.tol_f, cfg.max_evaluations or 400 * n,
+                                 cfg.restarts, P(best), C.byref(bf), C.byref(it), C.byref(ev),
+                                 C.byref(conv), P(fail))
+    if rc == 100:                          # MUSR_NM_RAISED: re-evaluate there, raising as the reference
+        reduced(fail)
+        raise RuntimeError("native Nelder-Mead reported an error the objective did not raise")
+    _check(rc, sess._handle, "musr_minimize")
+    full[free] = best
+    return FitResult(params.copy_with(full), bf.value, it.value, ev.value, bool(conv.value))
 
 
 def default_phases(n_detectors: int = 16) -> np.ndarray:

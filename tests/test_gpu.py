@@ -439,3 +439,37 @@ def test_long_parameter_vector_not_inline():
         fnb = pkg.chi2_batch if kind == "chi2" else pkg.mlh_batch
         fn = pkg.chi2 if kind == "chi2" else pkg.mlh
         assert list(fnb(dss, w.expr, P)) == [fn(dss, w.expr, p) for p in P]
+
+
+def test_native_minimize_identical_to_python_loop():
+    """pkg.minimize runs the Nelder-Mead loop natively (musr_minimize); the
+    Python loop over the same GPU objective gives the same fit bit for bit, and
+    an objective error raised mid-fit surfaces with the reference's message."""
+    w = workloads.c5(n_hist=4, nbins=1 << 16)
+    dss = workloads.synthesize(w)
+    start = pkg.ParameterSet(values=np.array([0.3, 0.15, 5.0, 0.045, 1000.0, 10.0]),
+                             names=["A0", "sigma", "phi", "B", "N0", "Nbkg"],
+                             step_sizes=np.array([0.01, 0.01, 1.0, 0.001, 1.0, 0.5]),
+                             bounds=[None, (1e-6, np.inf), None, (1e-6, np.inf), None, None],
+                             fixed=np.array([False, False, False, False, True, True]))
+    for kind, fn in (("chi2", pkg.chi2), ("mlh", pkg.mlh)):
+        native = pkg.minimize(kind, dss, w.expr, start)
+        loop = pkg.minimize(kind, dss, w.expr, start, objective_fn=lambda q: fn(dss, w.expr, q))
+        assert np.array_equal(native.best_parameters.values, loop.best_parameters.values), kind
+        assert native.objective_value == loop.objective_value
+        assert (native.iterations, native.objective_evaluations, native.converged) == \
+               (loop.iterations, loop.objective_evaluations, loop.converged)
+    # MLH turns non-positive mid-fit: the data fall faster than the envelope, the
+    # first reflection takes a below -1 / t_max and the model below zero
+    expr = pkg.parse("p[m[0]] * t")
+    t = np.arange(400000) * 0.001
+    counts = np.round(np.maximum(0.0, 50.0 * np.exp(-t / pkg.TAU_MU_US) * (1.0 - 0.003 * t)))
+    ds = pkg.MusrDataset(0, counts, 0.001, 0, pkg.TheoryBinding(map=(0,)), 1, 2)
+    bad = pkg.ParameterSet(values=np.array([0.0, 50.0, 0.0]), names=["a", "N0", "Nbkg"],
+                           step_sizes=np.array([0.01, 1.0, 1.0]),
+                           fixed=np.array([False, True, True]))
+    with pytest.raises(pkg.MusrError) as a:
+        pkg.minimize("mlh", [ds], expr, bad)
+    with pytest.raises(pkg.MusrError) as b:
+        pkg.minimize("mlh", [ds], expr, bad, objective_fn=lambda q: pkg.mlh([ds], expr, q))
+    assert str(a.value) == str(b.value)

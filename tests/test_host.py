@@ -364,3 +364,56 @@ def test_nelder_mead_identical_to_reference(ref):
             assert np.array_equal(c.x, b.x) and c.fun == b.fun
             assert (c.iterations, c.evaluations, c.converged) == (b.iterations, b.evaluations, b.converged)
             assert len(x0) == 1 or calls
+
+
+def _native_nm(fn, x0, steps, lo, hi, tol_f=1e-9, budget=0, restarts=1):
+    """musr_nm_run (the native loop behind musr_minimize) over a Python objective."""
+    lib = _lib.load()
+    n = len(x0)
+    CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_int,
+                     C.POINTER(C.c_double))
+
+    def cb(user, xs, k, nn, fs):
+        for i in range(k):
+            fs[i] = float(fn(np.array(xs[i * nn:(i + 1) * nn])))
+        return 0
+
+    keep = CB(cb)
+    x0 = np.minimum(np.maximum(np.asarray(x0, float), lo), hi)
+    f0 = float(fn(x0))
+    d = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+    best, fail = np.zeros(n), np.zeros(n)
+    bf, it, ev, conv = C.c_double(), C.c_int64(), C.c_int64(), C.c_int()
+    P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    a = [d(x0), d(steps), d(lo), d(hi)]
+    rc = lib.musr_nm_run(n, P(a[0]), f0, P(a[1]), P(a[2]), P(a[3]), tol_f, budget or 400 * n,
+                         restarts, C.cast(keep, C.c_void_p), None, P(best), C.byref(bf),
+                         C.byref(it), C.byref(ev), C.byref(conv), P(fail))
+    assert rc == 0
+    return best, bf.value, it.value, ev.value, bool(conv.value)
+
+
+@pytest.mark.parametrize("case", ["rosen2", "rosen5_bounded", "bowl_budget", "nan_region", "one_d"])
+def test_native_nelder_mead_bitwise_equal_to_python(case):
+    """The native loop (musr_minimize's core) reproduces optimize.nelder_mead
+    bit for bit: iterates, values, iteration and evaluation counts."""
+    from paper_1604_02334_b200.optimize import MinimizeConfig, nelder_mead
+
+    rosen = lambda x: float(np.sum(100.0 * (x[1:] - x[:-1] ** 2) ** 2 + (1 - x[:-1]) ** 2))
+    cfgs = {
+        "rosen2": (rosen, [-1.2, 1.0], [0.1, 0.1], [-np.inf] * 2, [np.inf] * 2, 0),
+        "rosen5_bounded": (rosen, [0.5, 0.2, -0.3, 1.5, 0.9], [0.2] * 5, [-1.0, 0.1, -2, 0.5, 0.0],
+                           [1.5, 3.0, 2.0, 1.2, 2.0], 0),
+        "bowl_budget": (lambda x: float(np.dot(x - 3.0, x - 3.0)), [0.0, 10.0, -4.0], [1.0, 0.5, 2.0],
+                        [-np.inf] * 3, [np.inf] * 3, 37),
+        "nan_region": (lambda x: float("nan") if x[0] > 1.7 else float((x[0] - 2) ** 2 + x[1] ** 2),
+                       [0.0, 1.0], [0.6, 0.3], [-np.inf] * 2, [np.inf] * 2, 0),
+        "one_d": (lambda x: float(np.cos(x[0]) + 0.1 * x[0] ** 2), [2.0], [0.3], [-5.0], [5.0], 0),
+    }
+    fn, x0, steps, lo, hi, budget = cfgs[case]
+    lo, hi = np.asarray(lo, float), np.asarray(hi, float)
+    ref = nelder_mead(fn, x0, steps, lo, hi, MinimizeConfig(max_evaluations=budget))
+    best, bf, it, ev, conv = _native_nm(fn, x0, steps, lo, hi, budget=budget)
+    assert np.array_equal(best.view(np.int64), ref.x.view(np.int64)), (best, ref.x)
+    assert (bf == ref.fun) or (np.isnan(bf) and np.isnan(ref.fun))
+    assert (it, ev, conv) == (ref.iterations, ref.evaluations, ref.converged)
