@@ -72,8 +72,18 @@ def _term(rng, depth=0):
     return f"-{_term(rng, depth + 1)}"
 
 
-def _case(i):
-    rng = np.random.default_rng(1000 + i)
+def _counts(rng, n, regime):
+    """Counts: typical (Poisson 50-900), low (Poisson 0.2-5: many zero bins, MLH's
+    d = 0 branch), or non-integer (the f64 data format)."""
+    if regime == "low":
+        return rng.poisson(rng.uniform(0.2, 5.0), n)
+    if regime == "real":
+        return rng.uniform(0.0, 300.0, n)
+    return rng.poisson(rng.uniform(50, 900), n)
+
+
+def _case(i, regime="typical"):
+    rng = np.random.default_rng(1000 + i + (0 if regime == "typical" else 7919 * len(regime)))
     src = f"p[m[0]] * ({_term(rng)})"
     if rng.random() < 0.6:
         src += f" + p[m[1]] * ({_term(rng, 1)})"
@@ -82,7 +92,7 @@ def _case(i):
     for j in range(int(rng.integers(1, 4))):
         n = int(rng.choice([1, 777, 4096, 4097, 20000]))
         m = tuple(int(x) for x in rng.permutation(6))
-        ds = pkg.MusrDataset(j, rng.poisson(rng.uniform(50, 900), n), 10.0 / max(n, 100),
+        ds = pkg.MusrDataset(j, _counts(rng, n, regime), 10.0 / max(n, 100),
                              int(rng.integers(0, 4)) if n > 10 else 0, pkg.TheoryBinding(
                                  map=m, function_values=tuple(float(x) for x in rng.uniform(0, 1, 6))),
                              6, 7)
@@ -93,9 +103,13 @@ def _case(i):
     return src, expr, dss, p
 
 
-@pytest.mark.parametrize("i", range(N_CASES))
-def test_random_theories_match_oracle(i):
-    src, expr, dss, p = _case(i)
+CASES = [(i, "typical") for i in range(N_CASES)] + [(i, "low") for i in range(10)] + \
+        [(i, "real") for i in range(6)]
+
+
+@pytest.mark.parametrize("i,regime", CASES)
+def test_random_theories_match_oracle(i, regime):
+    src, expr, dss, p = _case(i, regime)
     for kind in ("chi2", "mlh"):
         fn, ofn = (pkg.chi2, O.chi2) if kind == "chi2" else (pkg.mlh, O.mlh)
         try:
