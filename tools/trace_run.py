@@ -33,9 +33,9 @@ for kind in (0, 1):
     cols = [("start", rel[:, 0]), ("rows done", ext_rel[:, 0]), ("rows barrier", ext_rel[:, 1]),
             ("after prologue", rel[:, 1]), ("1st data", ext_rel[:, 2]), ("1st tile done", ext_rel[:, 3]),
             ("producer exit", rel[:, 3])]
-    prod = np.array(buf[8 * n.value: 16 * n.value], dtype=np.int64).reshape(-1, 8)[:, :6].astype(float)
+    prod = np.array(buf[8 * n.value: 16 * n.value], dtype=np.int64).reshape(-1, 8).astype(float)
     tiles_cta = tiles.astype(float)
-    names = ["wait idx", "wait done", "fold", "grab", "issue", "rest"]
+    names = ["wait idx", "wait done", "fold", "grab", "publish", "rest", "tma", "grab-ahead"]
     tot = prod.sum(axis=1)
     print("  producer cycles per tile (median over CTAs): " + ", ".join(
         f"{nm} {np.median(prod[:, k] / np.maximum(tiles_cta, 1)):.0f}" for k, nm in enumerate(names)) +
