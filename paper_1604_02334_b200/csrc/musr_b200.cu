@@ -1211,7 +1211,8 @@ int musr_debug_trace(musr_ctx* c, int kind, uint64_t* out, int cap, int* n_ctas)
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   // [grid][4] basic stamps, then (if cap allows) [grid][4] prologue / first-tile stamps
   const int n = std::min<int>(cap / 4, (int)c->grid[kind]);
-  const size_t words = (cap >= 16 * (int)c->grid[kind]) ? (size_t)16 * n
+  const size_t words = (cap >= 20 * (int)c->grid[kind]) ? (size_t)20 * n
+                       : (cap >= 16 * (int)c->grid[kind]) ? (size_t)16 * n
                        : (cap >= 8 * (int)c->grid[kind]) ? (size_t)8 * n : (size_t)4 * n;
   CUDA_TRY(c, cudaMemcpy(out, c->trace, words * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   *n_ctas = n;

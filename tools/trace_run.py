@@ -40,6 +40,14 @@ for kind in (0, 1):
     print("  producer cycles per tile (median over CTAs): " + ", ".join(
         f"{nm} {np.median(prod[:, k] / np.maximum(tiles_cta, 1)):.0f}" for k, nm in enumerate(names)) +
         f"; total {np.median(tot / np.maximum(tiles_cta, 1)):.0f}")
+    s2 = np.array(buf[16 * n.value: 20 * n.value], dtype=np.int64).reshape(-1, 4)
+    has = s2[:, 2] > 0
+    if has.any():
+        rel2 = (s2[has, 1:].astype(float) - t0) / 1e3
+        order2 = np.argsort(rel2[:, 2])[-4:]
+        print("  latest stage-2 runs (check, start, end us; CTA exit us): " + "; ".join(
+            f"{rel2[i, 0]:.1f} {rel2[i, 1]:.1f} {rel2[i, 2]:.1f} (exit {ex[np.flatnonzero(has)[i]]:.1f})"
+            for i in order2))
     for label, v in cols:
         v = v[~np.isnan(v)]
         if len(v):
