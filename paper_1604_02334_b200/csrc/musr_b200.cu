@@ -95,6 +95,7 @@ struct DriverApi {
   CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
   CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*ModuleGetGlobal)(CUdeviceptr*, size_t*, CUmodule, const char*) = nullptr;
+  CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
 };
 std::mutex g_drv_mu;
 DriverApi g_drv;
@@ -113,6 +114,7 @@ bool load_driver(std::string* err) {
        (void**)&d.OccupancyMaxActiveBlocksPerMultiprocessor},
       {"cuFuncSetAttribute", (void**)&d.FuncSetAttribute},
       {"cuModuleGetGlobal", (void**)&d.ModuleGetGlobal},
+      {"cuFuncGetAttribute", (void**)&d.FuncGetAttribute},
   };
   for (auto& s : syms) {
     cudaDriverEntryPointQueryResult q;
@@ -451,8 +453,15 @@ constexpr int kTableMax = 4096;         // c32 format: counts must be integers <
 // bytes of extra per stage (batched thread-node blocks).  0 if none fits.
 int fit_stages(CUfunction fn, int threads, size_t stage, size_t per_stage, size_t extra,
                int max_stages, size_t* smem_out, int* occ_out) {
+  // candidates beyond the opt-in limit (minus the kernel's static shared
+  // memory) are skipped without asking the driver (no failing API calls)
+  int dev = 0, optin = 0, stat = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  g_drv.FuncGetAttribute(&stat, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, fn);
   for (int st = max_stages; st >= 1; --st) {
     const size_t smem = (size_t)st * (stage + per_stage) + extra;
+    if (optin > 0 && smem + (size_t)stat > (size_t)optin) continue;
     if (g_drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) !=
         CUDA_SUCCESS)
       continue;
