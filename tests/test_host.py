@@ -417,3 +417,31 @@ def test_native_nelder_mead_bitwise_equal_to_python(case):
     assert np.array_equal(best.view(np.int64), ref.x.view(np.int64)), (best, ref.x)
     assert (bf == ref.fun) or (np.isnan(bf) and np.isnan(ref.fun))
     assert (it, ev, conv) == (ref.iterations, ref.evaluations, ref.converged)
+
+
+def test_native_nelder_mead_reports_failing_point():
+    """A nonzero status from the objective aborts the native loop with that
+    status and the failing point in fail_x (musr_minimize re-raises there)."""
+    lib = _lib.load()
+    CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_int,
+                     C.POINTER(C.c_double))
+    seen = []
+
+    def cb(user, xs, k, n, fs):
+        for i in range(k):
+            x = [xs[i * n + j] for j in range(n)]
+            seen.append(x)
+            if len(seen) == 5:
+                return 100
+            fs[i] = (x[0] - 1.0) ** 2 + (x[1] + 2.0) ** 2
+        return 0
+
+    keep = CB(cb)
+    P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    x0, st = np.array([0.0, 0.0]), np.array([0.5, 0.5])
+    lo, hi = np.full(2, -np.inf), np.full(2, np.inf)
+    best, fail = np.zeros(2), np.zeros(2)
+    rc = lib.musr_nm_run(2, P(x0), 5.0, P(st), P(lo), P(hi), 1e-9, 800, 1,
+                         C.cast(keep, C.c_void_p), None, P(best), None, None, None, None, P(fail))
+    assert rc == 100
+    assert fail.tolist() == seen[4]
