@@ -48,6 +48,7 @@ extern "C" {
 #define MUSR_ERR_NOMEM 5    /* device or pinned allocation failed        */
 
 #define MUSR_ERR_IO 6       /* muSR data file: see musr_io_error.code     */
+#define MUSR_ERR_PEER 7     /* shared results: a peer rank died, closed or timed out */
 
 #define MUSR_KIND_CHI2 0
 #define MUSR_KIND_MLH 1
@@ -87,11 +88,21 @@ int musr_open_sharded(int device, int rank, int world, const char* nccl_lib,
  * host reads every dataset's result directly -- the per-evaluation exchange
  * rides on the stage-2 stores, no ncclAllReduce and no device sync.  Double-
  * buffered by epoch parity.  `epoch_base` must differ between the handles
- * sharing a buffer (same value on every rank).  At most 64 datasets per rank.
+ * sharing a buffer (same value on every rank).  The last 8 * world bytes of
+ * `buf` hold each rank's process id while it has a handle open: a rank waiting
+ * for a peer's results fails with MUSR_ERR_PEER as soon as that peer exited or
+ * closed, or after MUSR_PEER_TIMEOUT_S seconds (environment, default 60).
  * Replaces the reference's single-process dataset loop (musr.py:190-201) for
  * sharded runs; values are bitwise identical to one GPU. */
 int musr_open_shared(int device, int rank, int world, void* buf, size_t bytes,
                      unsigned long long epoch_base, musr_ctx** out);
+
+/* Host half of the shared-results exchange, exposed for host-only tests: decode
+ * n_global datasets' LL words (4 per dataset, (32-bit half << 32) | epoch, as the
+ * objective kernel writes them) of evaluation `epoch` and fold them exactly as
+ * musr_eval does (musr.py:190-201).  MUSR_ERR_PEER if any word is stale. */
+int musr_collect_results(const unsigned long long* words, int n_global, unsigned epoch,
+                         double* per_dataset, int64_t* first_bad_bin, double* total);
 
 void musr_close(musr_ctx* ctx);
 const char* musr_last_error(const musr_ctx* ctx);
@@ -144,20 +155,6 @@ int musr_eval(musr_ctx* ctx, int kind, const double* p, int n_p, double* per_dat
 int musr_eval_batch(musr_ctx* ctx, int kind, const double* p, int n_points, int n_p,
                     double* per_dataset, int64_t* first_bad_bin, double* totals);
 
-/* Timing helpers (CUDA events on the handle's stream).
- *   mode 0: `iters` back-to-back graph replays (full evaluation incl. H2D p and
- *           D2H results, no host sync in between) -> *ms = total elapsed.
- *   mode 1: `iters` objective-kernel launches, each bracketed by its own
- *           events -> *ms = *kernel_ms = summed kernel time.
- *   mode 2: `iters` graph replays, each bracketed by events -> *ms = summed
- *           evaluation time, *kernel_ms = summed time of the objective kernel
- *           inside those same replays (event nodes captured in the graph).
- *   mode 3: no evaluation -- only the L2 flush below, then a stream sync (the
- *           caller times an end-to-end call right after it).
- *   flush_l2 (modes 1, 2, 3): 1 = write 512 MiB before each iteration, outside the
- *   timed interval, so inputs never start L2-resident; 2 = that, then read
- *   256 MiB of it back, so the L2 also holds no dirty lines whose write-back
- *   would land inside the timed interval. */
 /* Datasets of the whole (possibly sharded) problem after musr_upload. */
 int musr_n_datasets(const musr_ctx* ctx, int* n_global);
 
@@ -190,6 +187,25 @@ int musr_nm_run(int n, const double* x0, double f0, const double* step, const do
                 void* user, double* best_x, double* best_f, int64_t* iterations,
                 int64_t* evaluations, int* converged, double* fail_x);
 
+/* Timing helpers (CUDA events on the handle's stream).
+ *   mode 0: `iters` back-to-back graph replays (full evaluation incl. H2D p and
+ *           D2H results, no host sync in between) -> *ms = total elapsed.
+ *   mode 1: `iters` objective-kernel launches, each bracketed by its own
+ *           events -> *ms = *kernel_ms = summed kernel time.
+ *   mode 2: `iters` graph replays, each bracketed by events -> *ms = summed
+ *           evaluation time, *kernel_ms = summed time of the objective kernel
+ *           inside those same replays (event nodes captured in the graph).
+ *   mode 3: no evaluation -- only the L2 flush below, then a stream sync (the
+ *           caller times an end-to-end call right after it).
+ *   mode 4: `iters` synchronous evaluations at the last parameter vector
+ *           (musr_eval: launch, host waits for every dataset's result -- all
+ *           ranks' with shared results -- and folds).  Without a flush one event
+ *           pair spans all of them (launches, kernels and host waits); with a
+ *           flush each evaluation has its own pair and *ms is their sum.
+ *   flush_l2 (modes 1-4): 1 = write 512 MiB before each iteration, outside the
+ *   timed interval, so inputs never start L2-resident; 2 = that, then read
+ *   256 MiB of it back, so the L2 also holds no dirty lines whose write-back
+ *   would land inside the timed interval. */
 int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, double* ms,
                     double* kernel_ms);
 

@@ -29,6 +29,7 @@ from .musr import (  # noqa: F401
     minimize,
     mlh,
     mlh_batch,
+    uninstall,
 )
 from .objective import DeviceBackend, Session, shard_assignment  # noqa: F401
 from .optimize import MinimizeConfig, MinimizeResult, OptimizeError, nelder_mead  # noqa: F401

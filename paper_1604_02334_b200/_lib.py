@@ -40,6 +40,8 @@ SIGNATURES = [
      [C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
     ("musr_open_shared", C.c_int,
      [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("musr_collect_results", C.c_int,
+     [C.POINTER(C.c_uint64), C.c_int, C.c_uint, _DP, _I64P, _DP]),
     ("musr_close", None, [C.c_void_p]),
     ("musr_last_error", C.c_char_p, [C.c_void_p]),
     ("musr_set_theory", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_size_t]),

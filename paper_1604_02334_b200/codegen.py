@@ -354,9 +354,9 @@ class _VecEmitter:
     def _call(self, name: str, node: Call) -> None:
         arg = node.args[0]
         if node.name == "exp":
-            x = self.vec(arg) if not self.uniform_of(arg) else None
-            if x is None:  # cannot happen: uniform calls are hoisted
+            if self.uniform_of(arg):  # cannot happen: uniform calls are hoisted
                 raise TheoryError("uniform exp reached the vector emitter")
+            x = "t" if isinstance(arg, TimeVar) else self.vec(arg)
             self.lines.append(f"  {name}[0] = musr_exp_fast({x}[0], ok);")
             self._loop(name, f"musr_exp_anchored({x}[j], {x}[0], {name}[0], ok)", first=1)
         elif node.name in ("cos", "sin") and self.rotations is not None and arg in self.rotations:

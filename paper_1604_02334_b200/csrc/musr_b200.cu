@@ -17,6 +17,10 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nvrtc.h>
+#include <signal.h>
+#include <unistd.h>
+
+#include <cerrno>
 
 #include <cstdarg>
 #include <cstdio>
@@ -369,7 +373,9 @@ void free_data(musr_ctx* c) {
 // Direct-launch path: single GPU, per-dataset rows staged per CTA.  One
 // kernel launch per evaluation, parameters inline in the kernel parameters,
 // results written straight to mapped pinned host memory.
-bool direct_mode(const musr_ctx* c) { return c->comm == nullptr && c->n_local <= kMaxStaged; }
+// (Any number of datasets: beyond kMaxStaged the launch is preceded by the
+// uniform-table kernel, since the per-CTA rows no longer fit shared memory.)
+bool direct_mode(const musr_ctx* c) { return c->comm == nullptr; }
 
 MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   MusrArgs a;
@@ -689,12 +695,41 @@ int musr_open_sharded(int device, int rank, int world, const char* nccl_lib,
 static std::mutex g_shared_mu;
 static std::map<void*, int> g_shared_refs;
 
+// Liveness table at the end of a shared result buffer: one 8-byte word per
+// rank holding its process id while the rank has a handle open on the buffer
+// (0 = none).  A rank waiting for another rank's results checks it, so a peer
+// that died or closed its handle is reported at once instead of after the
+// timeout.
+static volatile unsigned long long* shared_pids(void* buf, size_t bytes, int world) {
+  return reinterpret_cast<volatile unsigned long long*>(static_cast<char*>(buf) + bytes) - world;
+}
+
+// 0: rank `r`'s process is alive with a handle on the buffer; else a reason.
+static const char* peer_gone(const musr_ctx* c, int r) {
+  const unsigned long long pid = shared_pids(c->shared_host, c->shared_bytes, c->world)[r];
+  if (pid == 0) return "has no open handle on the shared result buffer";
+  if (kill((pid_t)pid, 0) != 0 && errno == ESRCH) return "has exited";
+  char path[64], buf[256];
+  std::snprintf(path, sizeof(path), "/proc/%llu/stat", pid);
+  if (FILE* f = std::fopen(path, "r")) {
+    const size_t n = std::fread(buf, 1, sizeof(buf) - 1, f);
+    std::fclose(f);
+    buf[n] = 0;
+    const char* q = std::strrchr(buf, ')');
+    if (q && q[1] == ' ' && (q[2] == 'Z' || q[2] == 'X')) return "has exited (zombie)";
+  }
+  return nullptr;
+}
+
 int musr_open_shared(int device, int rank, int world, void* buf, size_t bytes,
                      unsigned long long epoch_base, musr_ctx** out) {
   if (world < 1 || rank < 0 || rank >= world)
     return set_err(nullptr, MUSR_ERR_ARG, fmt("bad rank %d / world %d", rank, world));
-  if (!buf || bytes < 64 || (reinterpret_cast<uintptr_t>(buf) & 63))
-    return set_err(nullptr, MUSR_ERR_ARG, "shared result buffer must be 64-byte aligned, >= 64 B");
+  if (!buf || bytes < 64 + (size_t)8 * world || (reinterpret_cast<uintptr_t>(buf) & 63) ||
+      (bytes & 7))
+    return set_err(nullptr, MUSR_ERR_ARG,
+                   "shared result buffer must be 64-byte aligned, a multiple of 8 bytes and hold "
+                   ">= 64 bytes plus one 8-byte word per rank");
   musr_ctx* c = nullptr;
   int rc = open_common(device, out, &c);
   if (rc != MUSR_OK) return rc;
@@ -723,6 +758,7 @@ int musr_open_shared(int device, int rank, int world, void* buf, size_t bytes,
   c->epoch_base = epoch_base;
   c->rank = rank;
   c->world = world;
+  shared_pids(buf, bytes, world)[rank] = (unsigned long long)getpid();
   *out = c;
   return MUSR_OK;
 }
@@ -736,6 +772,7 @@ void musr_close(musr_ctx* c) {
     std::lock_guard<std::mutex> lk(g_shared_mu);
     if (--g_shared_refs[c->shared_host] == 0) {
       g_shared_refs.erase(c->shared_host);
+      if (c->shared_bytes) shared_pids(c->shared_host, c->shared_bytes, c->world)[c->rank] = 0;
       cudaHostUnregister(c->shared_host);
     }
   }
@@ -891,10 +928,7 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
   if (n_global < 1 || n_local < 0 || n_local > n_global)
     return set_err(c, MUSR_ERR_ARG, fmt("bad dataset counts %d/%d", n_local, n_global));
   if (c->shared_host) {
-    if (n_local > kMaxStaged)
-      return set_err(c, MUSR_ERR_ARG, fmt("shared results take at most %d datasets per rank (%d); "
-                                          "use the NCCL-sharded handle", kMaxStaged, n_local));
-    if ((size_t)2 * 4 * 8 * n_global > c->shared_bytes)
+    if ((size_t)2 * 4 * 8 * n_global + (size_t)8 * c->world > c->shared_bytes)
       return set_err(c, MUSR_ERR_ARG, fmt("shared result buffer of %zu bytes is too small for "
                                           "%d datasets", c->shared_bytes, n_global));
   }
@@ -1102,6 +1136,32 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
 
 namespace {
 
+// One dataset's four LL words (sum hi, lo, bad hi, lo; musr_kernel.cuh
+// musr_ll_put) -> its sum and (first bad bin + 1, 0 = none).
+void ll_decode(const unsigned long long* x, double* sum, double* bad) {
+  const unsigned long long s = ((x[0] >> 32) << 32) | (x[1] >> 32);
+  const unsigned long long b = ((x[2] >> 32) << 32) | (x[3] >> 32);
+  std::memcpy(sum, &s, 8);
+  std::memcpy(bad, &b, 8);
+}
+
+// Per-dataset outputs and the total: the left fold of musr.py:190-201
+// (total = 0.0; total += s_j in dataset order).  h = [sums | bad + 1].
+void fold_results(const double* h, int G, double* per_dataset, int64_t* first_bad_bin,
+                  double* total) {
+  double acc = 0.0;
+  for (int i = 0; i < G; ++i) {
+    const double s = h[i];
+    if (per_dataset) per_dataset[i] = s;
+    if (first_bad_bin) {
+      const double b = h[G + i];
+      first_bad_bin[i] = (b == 0.0) ? -1 : (int64_t)b - 1;
+    }
+    acc = acc + s;
+  }
+  if (total) *total = acc;
+}
+
 // Device work of one evaluation on the handle's stream (no host sync).
 //   direct path: [H2D p if it does not fit inline] + one objective launch
 //   graph path : one graph replay (H2D p, [uniform table], objective,
@@ -1113,7 +1173,7 @@ int launch_eval(musr_ctx* c, int kind, unsigned long long epoch = 0) {
     if (!inline_p)
       CUDA_TRY(c, cudaMemcpyAsync(c->P, c->h_p, sizeof(double) * c->p_capacity,
                                   cudaMemcpyHostToDevice, c->stream));
-    return launch_kernels(c, kind, false, true, c->last_p.data(), inline_p ? n_p : -1, epoch);
+    return launch_kernels(c, kind, true, true, c->last_p.data(), inline_p ? n_p : -1, epoch);
   }
   CUDA_TRY(c, cudaGraphLaunch(c->gexec[kind], c->stream));
   return MUSR_OK;
@@ -1162,9 +1222,11 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
     // Each local dataset's stage-2 writer stores its results as LL words
     // carrying this evaluation's epoch; the host reads them as they land
     // (no completion flag, no device-side fence), typically before the kernel
-    // has retired.  Bounded: after 1 s (120 s when other ranks' results are
-    // awaited) a stream sync (which reports errors), after which every word of
-    // this rank is current.
+    // has retired.  Bounded: after 1 s a stream sync (which reports this
+    // rank's errors), after which every word of this rank is current.  Other
+    // ranks' words (shared results) are then awaited while their processes are
+    // alive with a handle open on the buffer, up to MUSR_PEER_TIMEOUT_S
+    // (default 60 s) -- a peer that exited or closed is reported at once.
     const uint32_t e32 = (uint32_t)c->epoch;
     // shared results: every rank's datasets, in this epoch's half of the buffer
     const bool shared = c->shared_host != nullptr;
@@ -1172,44 +1234,68 @@ int musr_eval(musr_ctx* c, int kind, const double* p, int n_p, double* per_datas
     auto out_of = [&](int j) { return shared ? j : c->hist_host[j].out_index; };
     volatile unsigned long long* ll = c->ll_host + (shared ? (size_t)(c->epoch & 1ull) * 4 * G : 0);
     int i = 0, w = 0;
-    // other ranks may still be uploading or evaluating: a longer bound when shared
-    const auto t_start = std::chrono::steady_clock::now();
-    const auto bound = shared ? std::chrono::seconds(120) : std::chrono::seconds(1);
+    auto t_start = std::chrono::steady_clock::now();
+    bool synced = false;
+    static const double peer_s = [] {
+      const char* v = std::getenv("MUSR_PEER_TIMEOUT_S");
+      return v ? std::max(0.0, std::atof(v)) : 60.0;
+    }();
     for (long spin = 0; i < n_read; ++spin) {
       const int o = out_of(i);
       while (w < 4 && (uint32_t)ll[4 * o + w] == e32) ++w;
-      if (w == 4) { ++i; w = 0; }
-      if ((spin & 4095) == 4095 && std::chrono::steady_clock::now() - t_start > bound) break;
-    }
-    if (i < n_read) {
-      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-      for (int j = 0; j < n_read; ++j)
-        for (int q = 0; q < 4; ++q)
-          if ((uint32_t)ll[4 * out_of(j) + q] != e32)
-            return set_err(c, MUSR_ERR_CUDA, "evaluation finished without its results");
+      if (w == 4) { ++i; w = 0; continue; }
+      if ((spin & 4095) != 4095) continue;
+      const double waited =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      if (!synced && waited > 1.0) {
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // this rank's words are now final
+        synced = true;
+        t_start = std::chrono::steady_clock::now();
+        continue;
+      }
+      if (!synced) continue;
+      // the word still missing belongs to another rank (or the kernel failed silently)
+      bool mine = !shared;
+      for (int k = 0; shared && k < c->n_local; ++k) mine = mine || c->hist_host[k].out_index == o;
+      if (mine)
+        return set_err(c, MUSR_ERR_CUDA,
+                       fmt("evaluation finished without the result of dataset %d", o));
+      if ((spin & 65535) == 65535)
+        for (int r = 0; r < c->world; ++r)
+          if (r != c->rank)
+            if (const char* why = peer_gone(c, r))
+              return set_err(c, MUSR_ERR_PEER,
+                             fmt("rank %d %s: the result of dataset %d (epoch %u) never "
+                                 "arrived", r, why, o, e32));
+      if (waited > peer_s)
+        return set_err(c, MUSR_ERR_PEER,
+                       fmt("the result of dataset %d (epoch %u) did not arrive within %.0f s "
+                           "(MUSR_PEER_TIMEOUT_S): is every rank evaluating the same problem?",
+                           o, e32, peer_s));
     }
     for (int j = 0; j < n_read; ++j) {
       const int o = out_of(j);
-      const unsigned long long* x = (const unsigned long long*)ll + 4 * o;
-      const unsigned long long s = ((x[0] >> 32) << 32) | (x[1] >> 32);
-      const unsigned long long b = ((x[2] >> 32) << 32) | (x[3] >> 32);
-      std::memcpy(&c->h_out[o], &s, 8);
-      std::memcpy(&c->h_out[G + o], &b, 8);
+      ll_decode((const unsigned long long*)ll + 4 * o, &c->h_out[o], &c->h_out[G + o]);
     }
   } else {
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   }
-  double acc = 0.0;
-  for (int i = 0; i < G; ++i) {
-    const double s = c->h_out[i];
-    if (per_dataset) per_dataset[i] = s;
-    if (first_bad_bin) {
-      const double b = c->h_out[G + i];
-      first_bad_bin[i] = (b == 0.0) ? -1 : (int64_t)b - 1;
-    }
-    acc = acc + s;  // musr.py:190-201: total = 0.0; total += s_j in dataset order
+  fold_results(c->h_out, G, per_dataset, first_bad_bin, total);
+  return MUSR_OK;
+}
+
+int musr_collect_results(const unsigned long long* words, int n_global, unsigned epoch,
+                         double* per_dataset, int64_t* first_bad_bin, double* total) {
+  if (!words || n_global < 0) return set_err(nullptr, MUSR_ERR_ARG, "bad arguments");
+  std::vector<double> h((size_t)2 * n_global);
+  for (int o = 0; o < n_global; ++o) {
+    for (int w = 0; w < 4; ++w)
+      if ((uint32_t)words[4 * o + w] != (uint32_t)epoch)
+        return set_err(nullptr, MUSR_ERR_PEER,
+                       fmt("the result of dataset %d does not carry epoch %u", o, epoch));
+    ll_decode(words + 4 * o, &h[o], &h[n_global + o]);
   }
-  if (total) *total = acc;
+  fold_results(h.data(), n_global, per_dataset, first_bad_bin, total);
   return MUSR_OK;
 }
 
@@ -1338,7 +1424,10 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
   CUDA_TRY(c, cudaEventCreate(&e0));
   CUDA_TRY(c, cudaEventCreate(&e1));
   double total = 0.0, ktotal = 0.0;
-  if ((mode == 1 || mode == 2 || mode == 3) && flush_l2 && !c->flush) {
+  if (mode < 0 || mode > 4) return set_err(c, MUSR_ERR_ARG, "bad timing mode");
+  if (mode == 4 && c->last_p.empty() && c->p_capacity > 0)
+    c->last_p.assign((size_t)c->p_capacity, 0.0);
+  if ((mode == 1 || mode == 2 || mode == 3 || mode == 4) && flush_l2 && !c->flush) {
     c->flush_bytes = (size_t)512 << 20;  // > 126 MB L2
     CUDA_TRY(c, cudaMalloc(&c->flush, c->flush_bytes));
     CUDA_TRY(c, cudaFuncSetAttribute(musr_l2_flush, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1376,6 +1465,39 @@ int musr_time_evals(musr_ctx* c, int kind, int iters, int mode, int flush_l2, do
       total += f;
       ktotal += fk;
     }
+  } else if (mode == 4) {
+    // `iters` synchronous evaluations (musr_eval at the last parameter vector:
+    // launch, then the host waits for every dataset's result -- with shared
+    // results every rank's -- and folds).  Without a flush: one event before the
+    // first launch and one after the last evaluation, so the interval covers
+    // the launches, the kernels and the host waits between them.  With a flush
+    // (inputs smaller than L2): the flush runs untimed before each evaluation,
+    // which is bracketed by its own events.
+    const std::vector<double> p = c->last_p;
+    if (!flush_l2) CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+    for (int i = 0; i < iters; ++i) {
+      if (flush_l2) {
+        CUDA_TRY(c, flush(i));
+        CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+      }
+      const int rc = musr_eval(c, kind, p.data(), (int)p.size(), nullptr, nullptr, nullptr);
+      if (rc != MUSR_OK) return rc;
+      if (flush_l2) {
+        CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+        CUDA_TRY(c, cudaEventSynchronize(e1));
+        float f = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&f, e0, e1));
+        total += f;
+      }
+    }
+    if (!flush_l2) {
+      CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+      CUDA_TRY(c, cudaEventSynchronize(e1));
+      float f = 0.f;
+      CUDA_TRY(c, cudaEventElapsedTime(&f, e0, e1));
+      total = f;
+    }
+    ktotal = total;
   } else if (mode == 0) {
     CUDA_TRY(c, cudaEventRecord(e0, c->stream));
     for (int i = 0; i < iters; ++i) {

@@ -515,7 +515,16 @@ int musr_file_load(const char* path, int n_threads, musr_file** out, musr_io_err
     for (const Item& it : ck.items) {
       const int64_t line = line0 + it.line;
       if (it.key == K_DETECTOR) {
-        if (open_block && (rc = finish(cur)) != MUSR_OK) break;
+        if (open_block && (rc = finish(cur)) != MUSR_OK) {
+          // io.py:177-178: finish() runs inside the DETECTOR line's try, where the
+          // TheoryBinding ValueError of a negative map entry becomes that line's
+          // "malformed line" FormatError (at EOF it stays a TheoryError)
+          if (err->code == MUSR_IO_BAD_MAP) {
+            err->detector = -1;
+            rc = fail_line(MUSR_IO_MALFORMED, line, it.first_off, it.first_len);
+          }
+          break;
+        }
         open_block = false;
         if (it.bad) { rc = fail_line(MUSR_IO_MALFORMED, line, it.first_off, it.first_len); break; }
         cur = Block();

@@ -47,6 +47,7 @@ __all__ = [
     "minimize",
     "default_phases",
     "install",
+    "uninstall",
     "TAU_MU_US",
     "GAMMA_MU",
 ]
@@ -368,3 +369,15 @@ def install(musr_module, theory_module=None, backend: Optional[DeviceBackend] = 
     musr_module.OBJECTIVES["mlh"] = gpu_mlh
     _obj.clear_cache()
     return previous
+
+
+def uninstall(musr_module, previous) -> None:
+    """Undo ``install``: restore the registry entries it returned and this
+    package's own exception classes."""
+    musr_module.OBJECTIVES.clear()
+    musr_module.OBJECTIVES.update(previous)
+    _obj.ERRORS.musr = MusrError
+    from .theory import EvalError
+
+    _obj.ERRORS.eval = EvalError
+    _obj.clear_cache()

@@ -307,6 +307,7 @@ class Session:
         eval_error = eval_error or ERRORS.eval
         self.lowered = _lowered(_adopt_ast(expr))
         self._handle = None
+        self._lock = threading.Lock()
         lib = _lib.load()
 
         be = self.backend
@@ -414,7 +415,13 @@ class Session:
             _lib.check(rc, self._handle, "musr_eval")
 
     def evaluate(self, kind: int, p, datasets=None, musr_error: type = None) -> float:
-        """Objective value with the reference's error semantics."""
+        """Objective value with the reference's error semantics.  Calls on one
+        session are serialised (the handle and its result buffers are
+        single-owner; the reference objectives are pure and thread-safe)."""
+        with self._lock:
+            return self._evaluate(kind, p, musr_error)
+
+    def _evaluate(self, kind: int, p, musr_error: type = None) -> float:
         p = np.ascontiguousarray(p, dtype=np.float64)
         if len(p) != self.n_p:
             raise ValueError("parameter vector length differs from the session's")
@@ -438,6 +445,10 @@ class Session:
         pass over the histograms per MUSR_KMAX points (musr_eval_batch).  Row i
         equals ``evaluate(kind, P[i])`` bit for bit; if any row would raise,
         the exception of the first such row (in row order) is raised."""
+        with self._lock:
+            return self._evaluate_batch(kind, P, musr_error)
+
+    def _evaluate_batch(self, kind: int, P, musr_error: type = None) -> np.ndarray:
         P = np.ascontiguousarray(P, dtype=np.float64)
         if P.ndim != 2 or P.shape[1] != self.n_p:
             raise ValueError("P must be (n_points, n_p) with the session's n_p")
@@ -471,6 +482,7 @@ class Session:
         return tot
 
     _detectors: Optional[List[int]] = None
+    _frozen: list = []
 
     def per_dataset(self) -> np.ndarray:
         return self._sums.copy()
@@ -493,12 +505,21 @@ class Session:
         self._lib.musr_format(self._handle, C.byref(f), C.byref(ts))
         return "c32" if f.value == 1 else "f64"
 
+    def launches_per_eval(self) -> int:
+        """Kernels of this library per evaluation: the objective kernel, preceded
+        by the uniform-table kernel when the local datasets exceed the per-CTA
+        staging (64).  0 on a rank without datasets."""
+        if self.n_tiles() == 0:
+            return 0
+        return 1 + (len(self.local_indices) > 64)
+
     def n_tiles(self) -> int:
         n = C.c_int64(0)
         self._lib.musr_tiles(self._handle, C.byref(n))
         return n.value
 
     def close(self) -> None:
+        _FROZEN.release(self)
         if self._handle:
             self._lib.musr_close(self._handle)
             self._handle = None
@@ -520,7 +541,9 @@ _CACHE_LOCK = threading.Lock()
 def _signature(datasets, expr, tau_mu, n_p, backend) -> tuple:
     parts = []
     for ds in datasets:
-        parts.append((id(ds), id(ds.counts), ds.fit_range, ds.dt, ds.t0_bin, ds.binding,
+        fr = ds.fit_range
+        fr = None if fr is None else tuple(float(x) for x in fr)   # list / ndarray ranges
+        parts.append((id(ds), id(ds.counts), fr, ds.dt, ds.t0_bin, ds.binding,
                       ds.n0_slot, ds.nbkg_slot, ds.detector_index))
     return (tuple(parts), id(expr), getattr(expr, "source", None), tau_mu, n_p, backend)
 
@@ -533,6 +556,71 @@ _LAST = {"datasets": None}
 # skips the per-field comparison.  (Other dataset types -- the reference's own
 # -- are compared field by field on every call.)
 DATASET_MUTATIONS = [0]
+
+
+class _FrozenCounts:
+    """Counts arrays held by cached sessions are made read-only.
+
+    The reference reads ``ds.counts`` on every call (musr.py:196); a session
+    uploads it once.  So that an in-place edit (``ds.counts[7] += 1``) can never
+    be answered from a stale device copy, every counts array a cached session
+    was built from is flagged ``writeable = False`` while the session lives:
+    the edit raises at the write site.  A caller that re-enables writing
+    (``ds.counts.flags.writeable = True``) may edit the array; the next call
+    sees the flag, drops the session and rebuilds it from the current
+    contents.  Flags are restored when the last session using an array closes.
+    """
+
+    def __init__(self):
+        self._held: Dict[int, list] = {}        # id(array) -> [array, refs, was_writeable]
+        self._of: Dict[int, list] = {}          # id(session) -> arrays it froze
+        self._lock = threading.Lock()
+
+    def freeze(self, sess, arrays) -> None:
+        mine = []
+        with self._lock:
+            for a in arrays:
+                if not isinstance(a, np.ndarray) or any(a is b for b in mine):
+                    continue
+                ent = self._held.get(id(a))
+                if ent is None or ent[0] is not a:
+                    ent = [a, 0, bool(a.flags.writeable)]
+                    self._held[id(a)] = ent
+                    if ent[2]:
+                        try:
+                            a.flags.writeable = False
+                        except ValueError:
+                            pass
+                ent[1] += 1
+                mine.append(a)
+            self._of[id(sess)] = mine
+            sess._frozen = mine
+
+    def intact(self, sess) -> bool:
+        """No array of ``sess`` was made writable again since it was frozen."""
+        for a in sess._frozen:
+            if a.flags.writeable:
+                return False
+        return True
+
+    def release(self, sess) -> None:
+        with self._lock:
+            for a in self._of.pop(id(sess), ()):
+                ent = self._held.get(id(a))
+                if ent is None or ent[0] is not a:
+                    continue
+                ent[1] -= 1
+                if ent[1] == 0:
+                    del self._held[id(a)]
+                    if ent[2] and not a.flags.writeable:
+                        try:
+                            a.flags.writeable = True
+                        except ValueError:
+                            pass
+            sess._frozen = []
+
+
+_FROZEN = _FrozenCounts()
 
 
 def _unchanged(datasets, snaps) -> bool:
@@ -556,19 +644,27 @@ def session_for(datasets, expr, tau_mu: float, n_p: int, backend: DeviceBackend)
     last = _LAST
     if (last["datasets"] is datasets and last["expr"] is expr and last["tau"] == tau_mu
             and last["n_p"] == n_p and (last["backend"] is backend or last["backend"] == backend)
+            and last["ids"] == tuple(map(id, datasets))       # list edited in place
             and ((last["own"] and last["mutations"] == DATASET_MUTATIONS[0])
                  or _unchanged(datasets, last["snaps"]))
-            and last["session"]._handle):
+            and last["session"]._handle and _FROZEN.intact(last["session"])):
         return last["session"]          # fast path: same call site as last time
     key = _signature(datasets, expr, tau_mu, n_p, backend)
     with _CACHE_LOCK:
         hit = _CACHE.get(key)
+        if hit is not None and not _FROZEN.intact(hit[0]):
+            # a cached counts array was made writable again (and maybe edited):
+            # its device copy can be stale, so rebuild from the current contents
+            del _CACHE[key]
+            hit[0].close()
+            hit = None
         if hit is not None:
             _CACHE.move_to_end(key)
             _remember(datasets, expr, tau_mu, n_p, backend, hit[0])
             return hit[0]
     sess = Session(datasets, expr, tau_mu, n_p, backend)
     sess._detectors = [int(ds.detector_index) for ds in datasets]
+    _FROZEN.freeze(sess, [ds.counts for ds in datasets])
     pin = [(ds, ds.counts) for ds in datasets] + [expr]   # keep ids alive while cached
     with _CACHE_LOCK:
         _CACHE[key] = (sess, pin)
@@ -584,6 +680,7 @@ def _remember(datasets, expr, tau_mu, n_p, backend, sess) -> None:
     from .musr import MusrDataset
 
     _LAST.update(datasets=datasets, expr=expr, tau=tau_mu, n_p=n_p, backend=backend,
+                 ids=tuple(map(id, datasets)),
                  snaps=[_FIELDS(ds) for ds in datasets], session=sess,
                  own=all(type(ds) is MusrDataset for ds in datasets),
                  mutations=DATASET_MUTATIONS[0])

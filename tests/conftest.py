@@ -14,13 +14,18 @@ ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
-REF_SRC = Path("/root/reference/pkg/src")
+# The reference package: its source tree in the build container, or the copy
+# installed into the git-ignored baseline/_ref by tools/stage_reference.sh,
+# which travels to the GPU host with the snapshot.
+REF_SRC = next((d for d in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src"))
+                if (d / "blk" / "musr.py").exists()), Path("/root/reference/pkg/src"))
 GOLDEN = ROOT / "tests" / "golden"
 
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device and the built libmusr_b200.so")
-    config.addinivalue_line("markers", "ref: needs the reference package (/root/reference)")
+    config.addinivalue_line("markers", "ref: needs the reference package (baseline/_ref or "
+                                       "/root/reference)")
 
 
 def reference_available() -> bool:
@@ -31,7 +36,7 @@ def reference_available() -> bool:
 def ref():
     """The reference package modules (blk.musr, blk.theory, blk.backend, blk.optimize)."""
     if not reference_available():
-        pytest.skip("reference package not present (only in the build container)")
+        pytest.skip("reference package not present (run tools/stage_reference.sh)")
     if str(REF_SRC) not in sys.path:
         sys.path.insert(0, str(REF_SRC))
     import blk.backend
@@ -77,12 +82,37 @@ def build_case(case, arrays, mirror):
     return dss, mirror.parse(case["expr"]), p, hexf(case["tau_mu"])
 
 
+# Largest relative difference seen by rel() in this session (GPU vs oracle /
+# reference / golden), written to gpurun_out/parity_max_rel.json at the end.
+PARITY = {"max_rel": 0.0, "where": None, "count": 0, "bitwise": 0}
+
+
 def rel(a: float, b: float) -> float:
     if np.isnan(a) and np.isnan(b):
-        return 0.0
-    if a == b:
-        return 0.0
-    return abs(a - b) / max(abs(b), 1e-300)
+        r = 0.0
+    elif a == b:
+        r = 0.0
+    else:
+        r = abs(a - b) / max(abs(b), 1e-300)
+    PARITY["count"] += 1
+    PARITY["bitwise"] += int(r == 0.0)
+    if r > PARITY["max_rel"]:
+        import os
+
+        PARITY["max_rel"] = float(r)
+        PARITY["where"] = os.environ.get("PYTEST_CURRENT_TEST", "?")
+    return r
+
+
+def pytest_sessionfinish(session, exitstatus):
+    if PARITY["count"] == 0:
+        return
+    out = ROOT / "gpurun_out"
+    try:
+        out.mkdir(exist_ok=True)
+        (out / "parity_max_rel.json").write_text(json.dumps(PARITY, indent=1) + "\n")
+    except OSError:
+        pass
 
 
 @pytest.fixture(scope="session")

@@ -36,6 +36,8 @@ CASES = {
     "malformed_before_block_end": "DETECTOR 4\ndt 0.1\ncounts x\nDETECTOR 5\n",
     "negative_count": "DETECTOR 2\n" + HDR + "counts 1 2\n3 -4 5\n",
     "negative_map": "DETECTOR 2\ndt 0.1\nt0 0\nn0_slot 0\nnbkg_slot 1\nmap 0 -1\ncounts 1\n",
+    "negative_map_first_of_two": "DETECTOR 2\ndt 0.1\nt0 0\nn0_slot 0\nnbkg_slot 1\nmap 0 -1\n"
+                                 "counts 1\nDETECTOR 3\n" + HDR + "counts 4\n",
     "empty_histogram": "DETECTOR 2\n" + HDR + "counts\n",
     "dt_zero": "DETECTOR 2\ndt 0.0\nt0 0\nn0_slot 0\nnbkg_slot 1\nmap 0\ncounts 1\n",
     "dt_negative_second_block": "DETECTOR 0\n" + HDR + "counts 1\nDETECTOR 1\ndt -1\nt0 0\n"

@@ -12,6 +12,11 @@ Every case is evaluated by the reference's own ``blk.musr.chi2`` / ``mlh``
 * ``crit2_*``   acceptance criterion 2 problems (test_acceptance.py:170-225)
 * ``theory_*``  the C1/C2/C3 benchmark theories at small
                 sizes with t0 > 0 and explicit fit ranges
+* ``dsl_*``     per-bin ``log``, per-bin-exponent ``pow`` / ``^``, ``exp(t)``,
+                uniform-exponent squares (theory.py:91-98, 450-452)
+* ``bitwise_*`` transcendental-free theories over ragged lengths (1, 2, 4095,
+                4096, 4097, 65539) with t0 > 0 and fit ranges: every per-bin op is
+                correctly rounded, so GPU chi2 must equal them bit for bit
 * ``exact_*``   exact-value tests (test_musr.py:99-180, test_acceptance.py:228-255)
 * ``err_*``     error semantics (empty range, map errors, non-positive MLH,
                 literal division by zero, N0 slot out of bounds)
@@ -114,6 +119,40 @@ def main() -> None:
                 ds.fit_range = rng_fit
             pert = np.array(p) * (1.0 + 0.02 * rng.standard_normal(len(p)))
             record(f"theory_{name}_{variant}", src, dss, pert)
+
+    # -- DSL builtins on a per-bin argument: log, per-bin-exponent pow, exp(t) ---------
+    dsl = [
+        ("log", "p[m[0]] * log(1 + p[m[1]] * t)", [0.05, 0.7]),
+        ("pow_bin_exp", "p[m[0]] * pow(1 + t / 10, -p[m[1]] * t)", [0.3, 0.2]),
+        ("caret_bin_exp", "p[m[0]] * (t / 10) ^ (0.5 * t)", [0.2, 0.0]),
+        ("exp_t", "p[m[0]] * exp(t) / 10000 + p[m[1]] * log(2 + t)", [0.5, 0.02]),
+        ("sq_uniform", "p[m[0]] * sin(3 * t) ^ 2 + p[m[1]] * sqrt(t)", [0.2, 0.05]),
+    ]
+    for name, src, a in dsl:
+        expr = parse(src)
+        pv = np.array(a + [1000.0, 10.0])
+        truth = musr.ParameterSet(values=pv, names=[f"x{i}" for i in range(len(pv))],
+                                  step_sizes=np.ones(len(pv)))
+        bindings = [TheoryBinding(map=(0, 1)) for _ in range(2)]
+        dss = musr.generate_synthetic(truth, expr, bindings, [2] * 2, [3] * 2, nbins=6007,
+                                      dt=10.0 / 6007, seed=300)
+        dss[1].t0_bin = 5
+        dss[1].fit_range = (0.25, 9.0)
+        record(f"dsl_{name}", src, dss, pv * (1.0 + 0.01 * rng.standard_normal(len(pv))))
+
+    # -- transcendental-free theories (every per-bin op correctly rounded): the GPU
+    #    total must equal these bit for bit, which pins the reduction tree -----------
+    for name, src, a in [("affine", "p[m[0]] * t + p[m[1]]", [0.01, -0.02]),
+                         ("rational", "p[m[0]] / (1 + t)", [0.3, 0.0]),
+                         ("zero", "0", [0.0, 0.0])]:
+        pv = np.array(a + [1000.0, 10.0])
+        dss = []
+        for j, (n, t0, fr) in enumerate([(1, 0, None), (2, 0, None), (4095, 3, None),
+                                         (4096, 0, (0.001, 9.0)), (4097, 11, None),
+                                         (65539, 0, (0.5, 7.5))]):
+            cnt = np.random.default_rng(500 + j).poisson(900.0 * np.exp(-np.arange(n) / n) + 10)
+            dss.append(dataset(j, cnt, 10.0 / max(n, 100), t0, (0, 1), (), 2, 3, fit_range=fr))
+        record(f"bitwise_{name}", src, dss, pv, kinds=("chi2", "mlh"))
 
     # -- exact-value tests --------------------------------------------------------
     zero = "0 * t"

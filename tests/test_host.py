@@ -243,8 +243,21 @@ def test_shard_assignment_contiguous_balanced():
         assert loads.max() <= n.sum() / world + n.max()
 
 
+def _ll_words(value: float, epoch: int):
+    """The objective kernel's LL encoding of one fp64 result (musr_kernel.cuh
+    musr_ll_put): two 8-byte words (32-bit half << 32) | epoch."""
+    b = int(np.float64(value).view(np.uint64))
+    return [((b >> 32) << 32) | epoch, ((b & 0xffffffff) << 32) | epoch]
+
+
 def _gloo_worker(rank, world, port, q):
-    import torch
+    """One rank of the shared-results exchange with the product's own host code:
+    shard_assignment (which datasets this rank owns), shared_result_buffer (the
+    ranks' common mapping) and musr_collect_results (decode + the ordered fold
+    musr_eval runs).  Only the device kernel is stood in for: the rank's owned
+    datasets are summed by the oracle and written as the kernel's LL words."""
+    import ctypes
+
     import torch.distributed as dist
 
     from oracle import musr_oracle as O
@@ -254,22 +267,41 @@ def _gloo_worker(rank, world, port, q):
     rng = np.random.default_rng(11)
     expr = pkg.parse("p[m[0]] * sg(t, p[m[1]])")
     dss = [_ds(j, rng.poisson(300, int(rng.integers(500, 3000))), (2, 3)) for j in range(7)]
-    p = np.array([1000.0, 10.0, 0.25, 0.3])
+    G = len(dss)
     owner = objective.shard_assignment([len(d.counts) for d in dss], world)
-    vec = np.zeros(2 * len(dss))                 # sums | bad+1, one contributor per slot
-    for j, ds in enumerate(dss):
-        if owner[j] == rank:
-            vec[j] = O.chi2([ds], expr, p)
-    t = torch.from_numpy(vec)
-    dist.all_reduce(t)                           # stands in for the in-graph ncclAllReduce
-    total = 0.0
-    for s in t.numpy()[: len(dss)]:
-        total = total + s                        # musr.py:190-201 left fold
-    q.put((rank, total, O.chi2(dss, expr, p)))
+    addr, nbytes = objective.shared_result_buffer(dist, 1 << 16)
+    words = (ctypes.c_uint64 * (nbytes // 8)).from_address(addr)
+    lib = _lib.load()
+    out = []
+    for epoch in (5, 6, 7):                     # double-buffered by epoch parity
+        p = np.array([1000.0, 10.0, 0.25, 0.3 + 0.01 * epoch])
+        base = (epoch & 1) * 4 * G
+        for j, ds in enumerate(dss):
+            if owner[j] == rank:
+                w = _ll_words(O.chi2([ds], expr, p), epoch) + _ll_words(0.0, epoch)
+                for k in range(4):
+                    words[base + 4 * j + k] = w[k]
+        dist.barrier()
+        per = np.zeros(G)
+        bad = np.zeros(G, dtype=np.int64)
+        tot = C.c_double()
+        rc = lib.musr_collect_results(
+            ctypes.cast(ctypes.addressof(words) + 8 * base, C.POINTER(C.c_uint64)), G, epoch,
+            per.ctypes.data_as(C.POINTER(C.c_double)), bad.ctypes.data_as(C.POINTER(C.c_int64)),
+            C.byref(tot))
+        stale = lib.musr_collect_results(
+            ctypes.cast(ctypes.addressof(words) + 8 * base, C.POINTER(C.c_uint64)), G, epoch + 2,
+            None, None, None)
+        out.append((rc, tot.value, O.chi2(dss, expr, p), bool((bad == -1).all()), stale))
+        dist.barrier()
+    q.put((rank, out, sorted(set(owner))))
     dist.destroy_process_group()
 
 
 def test_sharded_combination_is_exact_gloo():
+    """Two gloo ranks combine their shards' results through the product's
+    shared buffer and fold: every rank's total equals the one-process value
+    bit for bit (each slot has exactly one writer; the fold order is fixed)."""
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -281,8 +313,11 @@ def test_sharded_combination_is_exact_gloo():
     res = [q.get(timeout=120) for _ in procs]
     for pr in procs:
         pr.join(timeout=60)
-    for rank, total, single in res:
-        assert total == single   # bitwise: every slot has exactly one non-zero contributor
+    assert res[0][2] == [0, 1]                    # both ranks own datasets
+    for rank, out, _ in res:
+        for rc, total, single, none_bad, stale in out:
+            assert rc == 0 and total == single and none_bad, rank
+            assert stale == 7                     # MUSR_ERR_PEER: words of another epoch
 
 
 def _shm_worker(rank, world, port, q):
@@ -445,3 +480,73 @@ def test_native_nelder_mead_reports_failing_point():
                          C.cast(keep, C.c_void_p), None, P(best), None, None, None, None, P(fail))
     assert rc == 100
     assert fail.tolist() == seen[4]
+
+
+# -- session cache (objective.session_for) with a stand-in for the device session ----
+
+class _StubSession:
+    built = 0
+
+    def __init__(self, datasets, expr, tau_mu, n_p, backend):
+        type(self).built += 1
+        self.n = len(datasets)
+        self._handle = object()
+        self._frozen = []
+
+    def close(self):
+        objective._FROZEN.release(self)
+        self._handle = None
+
+
+@pytest.fixture
+def stub_sessions(monkeypatch):
+    objective.clear_cache()
+    monkeypatch.setattr(objective, "Session", _StubSession)
+    _StubSession.built = 0
+    yield _StubSession
+    objective.clear_cache()
+
+
+def test_session_cache_sees_list_edits_and_unhashable_ranges(stub_sessions):
+    expr = pkg.parse("p[m[0]] * t")
+    dss = [_ds(j, np.arange(10.0) + j, (2,)) for j in range(3)]
+    be = objective.DeviceBackend()
+    s1 = objective.session_for(dss, expr, 2.197019, 3, be)
+    assert objective.session_for(dss, expr, 2.197019, 3, be) is s1 and stub_sessions.built == 1
+    dss.pop()                                             # same list object, edited in place
+    s2 = objective.session_for(dss, expr, 2.197019, 3, be)
+    assert s2 is not s1 and s2.n == 2
+    dss.append(dss[0])                                    # re-appending an existing dataset
+    assert objective.session_for(dss, expr, 2.197019, 3, be).n == 3
+    dss[1].fit_range = [0.1, 0.5]                         # list (the reference accepts any pair)
+    objective.session_for(dss, expr, 2.197019, 3, be)
+    dss[1].fit_range = np.array([0.1, 0.6])
+    objective.session_for(dss, expr, 2.197019, 3, be)
+
+
+def test_session_cache_freezes_counts_and_rebuilds_after_unfreeze(stub_sessions):
+    """The reference reads ds.counts on every call (musr.py:196): an in-place
+    edit of a cached array must never be answered from the stale device copy.
+    It raises at the write site; after an explicit unfreeze the next call
+    rebuilds from the current contents; flags are restored on eviction."""
+    expr = pkg.parse("p[m[0]] * t")
+    ds = _ds(0, np.arange(10.0), (2,))
+    be = objective.DeviceBackend()
+    s1 = objective.session_for([ds], expr, 2.197019, 3, be)
+    with pytest.raises(ValueError):
+        ds.counts[3] += 1.0
+    same = [ds]
+    assert objective.session_for(same, expr, 2.197019, 3, be) is s1
+    ds.counts.flags.writeable = True
+    ds.counts[3] += 1.0
+    s2 = objective.session_for(same, expr, 2.197019, 3, be)
+    assert s2 is not s1 and stub_sessions.built == 2 and not ds.counts.flags.writeable
+    objective.clear_cache()
+    assert ds.counts.flags.writeable
+    shared = np.arange(5.0)                               # one array under two sessions
+    a, b = _ds(0, shared, (2,)), _ds(1, shared, (2,))
+    a.counts = shared
+    b.counts = shared
+    objective.session_for([a], expr, 2.197019, 3, be)
+    objective.session_for([b], expr, 2.197019, 4, be)
+    assert not shared.flags.writeable
