@@ -293,7 +293,7 @@ def main():
     value0 = call(dss, expr, p, backend)                      # builds the session (JIT, upload)
     sess = objective.session_for(dss, expr, pkg.TAU_MU_US, len(p), backend)
     local_bins = sess.local_terms
-    stream_bytes = local_bins * (12 if sess.data_format() == "c32" else 32)
+    stream_bytes = local_bins * (12 if sess.data_format() == "c32" else 16)
     flush = needs_flush(w, world) or stream_bytes < 2 * L2_BYTES   # C4: >= 400 MB per rank
     launches = sess.launches_per_eval()
 

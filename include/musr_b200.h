@@ -124,7 +124,11 @@ int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t*
  *   first_bin[i]   first in-range bin; t0_bin[i]; dt[i]
  *   counts[i], errors[i], envelope[i]
  *                  host arrays of n_terms[i] doubles starting at first_bin[i]
- *                  (errors may be NULL: MLH-only handle)
+ *                  (errors may be NULL: MLH-only handle).  errors[i] must be
+ *                  the reference's MusrDataset.errors() = max(1, sqrt(counts))
+ *                  (musr.py:95-96): it marks the handle chi2-capable, and the
+ *                  device recomputes it bit for bit (correctly rounded sqrt)
+ *                  instead of streaming it.
  *   n0_slot[i], nbkg_slot[i]   parameter indices (already wrapped)
  *   maps           n_local * map_stride int32 (per-dataset map rows)
  *   fvals          n_local * f_stride doubles (per-dataset function values)
@@ -209,9 +213,10 @@ int musr_nm_run(int n, const double* x0, double f0, const double* step, const do
 int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, double* ms,
                     double* kernel_ms);
 
-/* Data format chosen at upload: 0 = f64 streams (32 B/bin for chi2),
- * 1 = c32 (integral counts < 4096: fp32 counts + fp64 envelope, 12 B/bin, with
- * a {err, 1/err} table of `table_size` entries in shared memory). */
+/* Data format chosen at upload: 0 = f64 (counts + envelope as fp64, 16 B/bin;
+ * chi2 computes err and 1/err per bin), 1 = c32 (integral counts < 2^23: fp32
+ * counts + fp64 envelope, 12 B/bin, with a {err, 1/err} table of `table_size`
+ * (<= 4096) entries in shared memory; larger counts computed per bin). */
 int musr_format(const musr_ctx* ctx, int* format, int* table_size);
 
 /* Number of tiles (units of 256*R terms) one evaluation processes here. */

@@ -4,8 +4,11 @@ Drop-in for the objective path of the reference package ``blk``
 (``pkg/src/blk/musr.py:181-232``): the theory DSL is parsed on the host,
 lowered to CUDA and JIT-compiled with NVRTC for sm_100a; one fused fp64
 kernel evaluates model, residual/log-likelihood term and the reference's
-pairwise reduction tree; evaluations replay a captured CUDA graph; datasets
-can be sharded over GPUs with one NCCL all-reduce per evaluation.
+pairwise reduction tree, one launch per evaluation with the parameters in the
+kernel arguments and the per-dataset results returned through mapped host
+memory.  Datasets can be sharded over GPUs (one process per GPU); the ranks
+exchange results through a host buffer they all map, or with one fp64 NCCL
+all-reduce per evaluation (``combine="nccl"``).
 
 The compute lives in ``libmusr_b200.so`` (C ABI: ``include/musr_b200.h``).
 There is no CPU fallback.

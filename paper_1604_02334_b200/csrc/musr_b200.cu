@@ -4,11 +4,18 @@
 //   * NVRTC JIT of (theory fragment + kernel template) for sm_100a, cached by
 //     source hash (the paper's runtime kernel generation);
 //   * device layout: per-dataset in-range segments packed into aligned
-//     2048-term tiles of three fp64 streams (counts, errors, envelope);
-//   * one CUDA graph per objective kind: H2D p -> objective kernel ->
-//     [ncclAllReduce of the 2*n_global result vector] -> D2H results,
-//     replayed once per evaluation (hides the per-call launch/upload latency
-//     the paper identifies);
+//     4096-term tiles, 16-byte-group transposed; formats c32 (integer counts
+//     < 2^23 as fp32 + fp64 envelope, {err, 1/err} from a count-indexed table,
+//     in-kernel beyond it) and f64 (counts and envelope as fp64, err and 1/err
+//     in-kernel) -- musr_layout.h, musr_kernel.cuh;
+//   * the direct path (one GPU, the default): one launch of the persistent
+//     objective kernel per evaluation, p inside the kernel parameters, results
+//     returned as epoch-tagged 8-byte words in mapped host memory (no graph,
+//     no copy, no stream sync);
+//   * multi-GPU: the shared-results path (every rank's kernel writes its
+//     datasets' words into one host buffer all ranks map) or the NCCL path
+//     (one CUDA graph per kind: objective kernel -> fp64 ncclAllReduce of the
+//     2*n_global result vector -> D2H);
 //   * the ordered left fold of per-dataset sums (musr.py:190-201).
 //
 // The handle is single-threaded, like the reference orchestration.
@@ -191,11 +198,10 @@ struct musr_ctx {
   int64_t n_tiles = 0;
   int p_capacity = 0;
   void* d = nullptr;            // fp64 or fp32 (c32 format)
-  double* e = nullptr;
-  double* rcp = nullptr;
   double* env = nullptr;
   double2* table = nullptr;
   int table_size = 0;
+  bool big_counts = false;      // c32: some count >= table_size
   int fmt = 0;                  // 0: f64 streams, 1: c32 (fp32 counts + err/rcp table)
   int* tile_hist = nullptr;
   MusrHist* hist = nullptr;
@@ -249,8 +255,7 @@ struct musr_ctx {
 // Tile layout of one stream (musr_kernel.cuh): tiles of cthreads*pt terms; inside
 // a tile the 16-byte group k*cthreads + t holds thread t's elements g*k .. g*k+g-1
 // (g = 16 / element size), so consumer reads are conflict-free LDS.128.
-// mode 0: fp64 copy, 1: fp32 (exact for the c32 format), 2: fp64 reciprocal
-// (__drcp_rn == IEEE 1.0/x, the Markstein divisor of musr_div_y).
+// mode 0: fp64 copy, 1: fp32 (exact for the c32 format).
 __global__ void musr_layout_stream(const double* __restrict__ src, void* __restrict__ dst,
                                    size_t terms, unsigned pt, unsigned cthreads, int mode) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -264,7 +269,7 @@ __global__ void musr_layout_stream(const double* __restrict__ src, void* __restr
   if (mode == 1)
     static_cast<float*>(dst)[i] = (float)v;
   else
-    static_cast<double*>(dst)[i] = (mode == 2) ? __drcp_rn(v) : v;
+    static_cast<double*>(dst)[i] = v;
 }
 
 // L2 flush for timing (writes > 126 MB).  A kernel rather than cudaMemset so
@@ -335,13 +340,13 @@ void free_graphs(musr_ctx* c) {
 
 void free_data(musr_ctx* c) {
   free_graphs(c);
-  void* dev[] = {c->d, c->e, c->rcp, c->env, c->table, c->tile_hist, c->hist, c->P, c->maps,
+  void* dev[] = {c->d, c->env, c->table, c->tile_hist, c->hist, c->P, c->maps,
                  c->fvals, c->partial, c->count, c->bad, c->out_send, c->out_recv, c->utab,
                  c->sched, c->P_batch};
   for (void* p : dev)
     if (p) cudaFree(p);
   c->d = nullptr;
-  c->e = c->rcp = c->env = nullptr;
+  c->env = nullptr;
   c->table = nullptr;
   c->table_size = 0;
   c->tile_hist = nullptr;
@@ -381,11 +386,10 @@ MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   MusrArgs a;
   std::memset(&a, 0, sizeof(a));
   a.d = c->d;
-  a.e = c->e;
-  a.rcp = c->rcp;
   a.env = c->env;
   a.table = c->table;
   a.table_size = c->table_size;
+  a.big_counts = c->big_counts ? 1 : 0;
   a.tile_hist = c->tile_hist;
   a.hist = c->hist;
   a.P = c->P;
@@ -452,7 +456,8 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
   return MUSR_OK;
 }
 
-constexpr int kTableMax = 4096;         // c32 format: counts must be integers < this
+constexpr int kTableMax = 4096;          // c32 chi2: {err, 1/err} table entries (64 KB)
+constexpr double kCompactMax = 8388608.0;  // c32 format: counts are integers < 2^23
 
 // Deepest TMA pipeline (<= max_stages) whose shared memory fits one CTA per SM:
 // `stage` bytes per stage plus `extra` (table, staged rows); `per_stage`
@@ -491,11 +496,9 @@ int plan_launch(musr_ctx* c) {
   const size_t tile = (size_t)32 * c->cwarps * c->per_thread;  // terms per tile
   const int threads = 32 * (c->cwarps + 1);
   for (int kind = 0; kind < 2; ++kind) {
-    // MusrGeom in musr_kernel.cuh: d | env | err | rcp
-    size_t stage = tile * (c->fmt ? 4 : 8) + tile * 8;
-    if (kind == 0 && c->fmt == 0) stage += 2 * tile * 8;
-    // mirrors the single stage of the f64 chi2 kernel in musr_kernel.cuh
-    const int max_st = (kind == 0 && c->fmt == 0 && tile * 32 > 96 * 1024) ? 1 : c->stages;
+    // MusrGeom in musr_kernel.cuh: d | env
+    const size_t stage = tile * (c->fmt ? 4 : 8) + tile * 8;
+    const int max_st = c->stages;
     size_t extra = 0;
     if (kind == 0 && c->fmt == 1) extra += (size_t)c->table_size * 16;
     size_t extra_rows = 0;
@@ -976,24 +979,28 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
     if (maps[i] < 0)
       return set_err(c, MUSR_ERR_ARG, "negative map entry");
 
-  // Format: c32 when every in-range count is an integer in [0, kTableMax).
+  // Format: c32 when every in-range count is an integer in [0, 2^23) (exact in
+  // fp32); the chi2 table covers counts below min(max count + 1, 4096) rounded
+  // up to a power of two, larger counts get err and 1/err in-kernel.
   double max_count = 0.0;
   bool compact = n_local > 0;
   for (int i = 0; compact && i < n_local; ++i) {
     const double* x = counts[i];
     for (int64_t k = 0; k < n_terms[i]; ++k) {
       const double v = x[k];
-      if (!(v >= 0.0 && v < (double)kTableMax && v == (double)(int)v)) { compact = false; break; }
+      if (!(v >= 0.0 && v < kCompactMax && v == (double)(int)v)) { compact = false; break; }
       if (v > max_count) max_count = v;
     }
   }
   if (const char* f = std::getenv("MUSR_FORMAT")) compact = compact && std::strcmp(f, "f64") != 0;
   c->fmt = compact ? 1 : 0;
   c->table_size = 0;
+  c->big_counts = false;
   if (compact) {
     int ts = 16;
-    while (ts <= (int)max_count) ts <<= 1;
+    while (ts < kTableMax && ts <= (int)max_count) ts <<= 1;
     c->table_size = ts;
+    c->big_counts = max_count >= (double)ts;
   }
 
   c->n_global = n_global;
@@ -1024,10 +1031,6 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
 #define ALLOC(ptr, bytes) \
   if ((rc = dalloc((void**)&(ptr), (bytes))) != MUSR_OK) return rc
   ALLOC(c->d, terms * (compact ? 4 : 8));
-  if (all_err && !compact) {
-    ALLOC(c->e, terms * 8);
-    ALLOC(c->rcp, terms * 8);
-  }
   if (compact) ALLOC(c->table, (size_t)c->table_size * 16);
   ALLOC(c->env, terms * 8);
   ALLOC(c->tile_hist, (size_t)tiles * 4);
@@ -1067,10 +1070,7 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
     double* stage = nullptr;
     CUDA_TRY(c, cudaMalloc(&stage, terms * 8 + 8));
     struct Job { void* dst; const double* const* src; int mode; };
-    const Job jobs[4] = {{c->d, counts, compact ? 1 : 0},
-                         {c->env, envelope, 0},
-                         {c->e, errors, 0},
-                         {c->rcp, errors, 2}};
+    const Job jobs[2] = {{c->d, counts, compact ? 1 : 0}, {c->env, envelope, 0}};
     int rc2 = MUSR_OK;
     for (const Job& job : jobs) {
       if (!job.dst) continue;
@@ -1081,8 +1081,6 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
                              cudaMemcpyHostToDevice, c->stream);
       }
       if (ce == cudaSuccess && terms > 0) {
-        // padding must stay finite for the reciprocal stream (1/0 = inf is fine:
-        // padded terms are masked in-kernel)
         musr_layout_stream<<<(unsigned)((terms + 255) / 256), 256, 0, c->stream>>>(
             stage, job.dst, terms, (unsigned)c->per_thread, (unsigned)(32 * c->cwarps), job.mode);
         ce = cudaGetLastError();

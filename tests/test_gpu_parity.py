@@ -90,7 +90,11 @@ def test_chi2_tree_bitwise_ragged(src):
         om, om_per = _per_oracle("mlh", dss, expr, p)
         assert rel(gm, om) <= TOL
         per_m = objective.session_for(dss, expr, pkg.TAU_MU_US, len(p), pkg.DeviceBackend()).per_dataset()
-        assert max(rel(a, b) for a, b in zip(per_m, om_per)) <= TOL
+        # a dataset of a few bins has no averaging: each MLH term (m - d) + d log(d/m)
+        # cancels ~30x, so one ulp of log is ~1e-14 of the term; the north star's
+        # per-histogram bound (1e-12) applies there, 1e-14 from 64 bins up
+        for n, a, b in zip(LENGTHS, per_m, om_per):
+            assert rel(a, b) <= (TOL if n >= 64 else 1e-12), (n, a, b)
     for ds in dss[3:8]:                       # one dataset per session: tile 0 is its first
         assert pkg.chi2([ds], expr, p).hex() == float(O.chi2([ds], expr, p)).hex()
 
@@ -134,6 +138,65 @@ def test_tree_bitwise_across_pipeline_depth_and_tile_order(monkeypatch):
         monkeypatch.setenv("MUSR_STAGES", st)
         objective.clear_cache()
         assert all(pkg.chi2(dss, expr, p).hex() == want for _ in range(3)), st
+
+
+# -- count formats: high-statistics integer counts and non-integer counts ---------------
+
+def _hi_datasets(lengths, n0, seed, fractional=False):
+    """Histograms whose early bins carry counts far beyond the 4096-entry
+    {err, 1/err} table (n0 up to ~8e6, still < 2^23), so one tile mixes table
+    lookups and in-kernel sqrt / reciprocal; ``fractional`` adds non-integer
+    counts (the f64 format)."""
+    rng = np.random.default_rng(seed)
+    dss = []
+    for j, n in enumerate(lengths):
+        dt = 10.0 / max(n, 64)
+        lam = n0 * np.exp(-np.arange(n) * dt / 2.197019) + 10.0
+        c = rng.poisson(lam).astype(np.float64)
+        if fractional:
+            c = c + rng.uniform(0.0, 1.0, n).round(3)
+        ds = pkg.MusrDataset(j, c, dt, int(rng.integers(0, 5)) if n > 8 else 0,
+                             pkg.TheoryBinding(map=(0, 1)), 2, 3)
+        if n > 100 and j % 3 == 1:
+            ds.fit_range = (float(0.05 * n * dt), float(0.93 * n * dt))
+        dss.append(ds)
+    return dss
+
+
+@pytest.mark.parametrize("n0,fractional,fmt", [(1e5, False, "c32"), (8.0e6, False, "c32"),
+                                              (3000.0, True, "f64"), (1e5, True, "f64")])
+def test_chi2_tree_bitwise_count_formats(n0, fractional, fmt):
+    """Counts beyond the table (err and 1/err computed per bin with the
+    correctly rounded sqrt / reciprocal) and non-integer counts (f64 format,
+    16 B/bin): chi2 still bit-identical to the oracle per dataset and in
+    total; MLH within 1e-14."""
+    expr = pkg.parse(THEORIES[0])
+    rng = np.random.default_rng(int(n0) % 1000 + fractional)
+    dss = _hi_datasets([4095, 4097, 70001, 1, 300000], n0, seed=21 + fractional)
+    p = _params(rng)
+    p[2] = n0
+    got = pkg.chi2(dss, expr, p)
+    sess = objective.session_for(dss, expr, pkg.TAU_MU_US, len(p), pkg.DeviceBackend())
+    assert sess.data_format() == fmt
+    want, want_per = _per_oracle("chi2", dss, expr, p)
+    assert _bits(sess.per_dataset()) == _bits(want_per)
+    assert got.hex() == float(want).hex()
+    assert rel(pkg.mlh(dss, expr, p), O.mlh(dss, expr, p)) <= TOL
+
+
+def test_high_statistics_c2_theory_matches_oracle():
+    """The C2 theory (Gaussian-relaxed TF precession) on N0 = 1e5 data: ~70 % of
+    the bins beyond the count table; chi2 and MLH within 1e-14."""
+    w = workloads.c2(n_hist=4, nbins=1 << 16)
+    for j in range(4):
+        w.params[3 + 3 * j + 1] = 1e5
+    dss = workloads.synthesize(w)
+    sess_fmt = None
+    for kind, fn, ofn in (("chi2", pkg.chi2, O.chi2), ("mlh", pkg.mlh, O.mlh)):
+        assert rel(fn(dss, w.expr, w.params), ofn(dss, w.expr, w.params)) <= TOL, kind
+        sess_fmt = objective.session_for(dss, w.expr, pkg.TAU_MU_US, len(w.params),
+                                         pkg.DeviceBackend()).data_format()
+    assert sess_fmt == "c32"
 
 
 # -- two ranks (processes) on this GPU, results through the shared host buffer -------
