@@ -1,12 +1,13 @@
 """Benchmark: fp64 chi2 (or MLH) evaluations of the uSR fit objective on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload C4|C1|C2|C3] [--objective chi2|mlh] [--combine host|nccl]
+                    [--workload C4|C1|C2|C2H|C3] [--objective chi2|mlh] [--combine host|nccl]
 
 The metric (BASELINE.json) is quoted on config C4 -- 64 histograms x 2^22 bins,
 Eq. 6 theory, sharded across 1/2/4/8 GPUs -- so C4 is the default workload at
 every N (strong scaling: the same 268 M bins split over the ranks).  C1-C3 are
-named extra workloads (single GPU).  Inputs are the reference generator's
+named extra workloads (single GPU); C2H is C2 at N0 = 1e5 (high-statistics
+counts, most beyond the count table).  Inputs are the reference generator's
 (``blk.musr.generate_synthetic``, SURVEY.md 8(d) seeds and shapes) when the
 reference is installed in baseline/_ref, else the package's restatement of it.
 
@@ -130,7 +131,7 @@ def build_workload(name: str):
     the package's own synthesis of the same shapes."""
     from paper_1604_02334_b200 import workloads as W
 
-    w = {"C1": W.c1, "C2": W.c2, "C3": W.c3, "C4": W.c4, "C5": W.c5}[name]()
+    w = W.WORKLOADS[name]()
     blk = reference_package()
     if blk is None:
         return w, W.synthesize(w), "paper_1604_02334_b200.workloads.synthesize"
@@ -166,7 +167,8 @@ def workload_config(args, w, world, flush):
                             + ("result exchange through a host buffer all ranks map (kernel "
                                "stage-2 stores, no device collective)" if args.combine == "host"
                                else "fp64 ncclAllReduce in the evaluation's CUDA graph"))
-            if world > 1 else "single GPU",
+            if world > 1 else ("single GPU" if args.combine == "host" else
+                               "single GPU, NCCL data plane (1-rank ncclAllReduce in the CUDA graph)"),
             "l2": ("flushed (512 MB write, untimed) before every timed step" if flush else
                    "inputs larger than L2 (no flush; steps back to back)")}
 
@@ -248,7 +250,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", default="C4", choices=("C1", "C2", "C3", "C4"))
+    ap.add_argument("--workload", default="C4", choices=("C1", "C2", "C2H", "C3", "C4"))
     ap.add_argument("--objective", default="chi2", choices=("chi2", "mlh"))
     ap.add_argument("--combine", default="host", choices=("host", "nccl"),
                     help="multi-GPU result exchange (N > 1)")
@@ -281,6 +283,8 @@ def main():
                                  "on one device); MUSR_BENCH_DEVICE checks the host path only")
             dist.init_process_group("gloo")
         backend = pkg.DeviceBackend.from_torch_distributed(local, combine=args.combine)
+    elif args.combine == "nccl":   # the NCCL data plane at world 1: graph (kernel + allreduce + D2H)
+        backend = pkg.DeviceBackend(device=local, collective=True, nccl_id=objective.new_nccl_id())
     else:
         backend = pkg.DeviceBackend(device=local)
 

@@ -5,7 +5,7 @@
 //     source hash (the paper's runtime kernel generation);
 //   * device layout: per-dataset in-range segments packed into aligned
 //     4096-term tiles, 16-byte-group transposed; formats c32 (integer counts
-//     < 2^23 as fp32 + fp64 envelope, {err, 1/err} from a count-indexed table,
+//     < 2^31 as int32 + fp64 envelope, {err, 1/err} from a count-indexed table,
 //     in-kernel beyond it) and f64 (counts and envelope as fp64, err and 1/err
 //     in-kernel) -- musr_layout.h, musr_kernel.cuh;
 //   * the direct path (one GPU, the default): one launch of the persistent
@@ -169,9 +169,9 @@ struct musr_ctx {
 
   // theory module
   CUmodule mod = nullptr;
-  CUfunction fn[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [kind][fmt]
+  CUfunction fn[2][3] = {};  // [kind][kernel format: 0 f64, 1 c32, 2 c32 + counts beyond the table]
   CUfunction fn_utab = nullptr;
-  CUfunction fn_batch[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // musr_eval_batch
+  CUfunction fn_batch[2][3] = {};  // musr_eval_batch
   bool have_theory = false;
   int n_uniform = 1;            // MUSR_NU of the loaded theory
   int sms = 0;                  // multiprocessors on the device
@@ -197,12 +197,12 @@ struct musr_ctx {
   int n_global = 0, n_local = 0;
   int64_t n_tiles = 0;
   int p_capacity = 0;
-  void* d = nullptr;            // fp64 or fp32 (c32 format)
+  void* d = nullptr;            // fp64, or int32 (c32 format)
   double* env = nullptr;
   double2* table = nullptr;
   int table_size = 0;
   bool big_counts = false;      // c32: some count >= table_size
-  int fmt = 0;                  // 0: f64 streams, 1: c32 (fp32 counts + err/rcp table)
+  int fmt = 0;                  // 0: f64 streams, 1: c32 (int32 counts + err/rcp table)
   int* tile_hist = nullptr;
   MusrHist* hist = nullptr;
   double* P = nullptr;
@@ -255,7 +255,7 @@ struct musr_ctx {
 // Tile layout of one stream (musr_kernel.cuh): tiles of cthreads*pt terms; inside
 // a tile the 16-byte group k*cthreads + t holds thread t's elements g*k .. g*k+g-1
 // (g = 16 / element size), so consumer reads are conflict-free LDS.128.
-// mode 0: fp64 copy, 1: fp32 (exact for the c32 format).
+// mode 0: fp64 copy, 1: int32 (the c32 format: integer counts < 2^31).
 __global__ void musr_layout_stream(const double* __restrict__ src, void* __restrict__ dst,
                                    size_t terms, unsigned pt, unsigned cthreads, int mode) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -267,7 +267,7 @@ __global__ void musr_layout_stream(const double* __restrict__ src, void* __restr
   const unsigned grp = r / g, e = r - grp * g, k = grp / cthreads, t = grp % cthreads;
   const double v = src[tile * tile_terms + (size_t)t * pt + g * k + e];
   if (mode == 1)
-    static_cast<float*>(dst)[i] = (float)v;
+    static_cast<int*>(dst)[i] = (int)v;
   else
     static_cast<double*>(dst)[i] = v;
 }
@@ -382,6 +382,11 @@ void free_data(musr_ctx* c) {
 // uniform-table kernel, since the per-CTA rows no longer fit shared memory.)
 bool direct_mode(const musr_ctx* c) { return c->comm == nullptr; }
 
+// Kernel variant for the data format: chi2 on c32 data with counts beyond the
+// {err, 1/err} table has its own entry point (the in-kernel sqrt / reciprocal
+// path would otherwise cost the common table-only kernel registers).
+int kfmt(const musr_ctx* c, int kind) { return (kind == 0 && c->fmt == 1 && c->big_counts) ? 2 : c->fmt; }
+
 MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   MusrArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -389,7 +394,6 @@ MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   a.env = c->env;
   a.table = c->table;
   a.table_size = c->table_size;
-  a.big_counts = c->big_counts ? 1 : 0;
   a.tile_hist = c->tile_hist;
   a.hist = c->hist;
   a.P = c->P;
@@ -451,13 +455,13 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
   if (with_table)
     CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (unsigned)((c->n_local + 3) / 4), 1, 1, 128, 1,
                                  1, 0, (CUstream)c->stream, params, nullptr));
-  CU_TRY(c, g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, 32 * (c->cwarps + 1), 1, 1,
+  CU_TRY(c, g_drv.LaunchKernel(c->fn[kind][kfmt(c, kind)], c->grid[kind], 1, 1, 32 * (c->cwarps + 1), 1, 1,
                                (unsigned)c->dyn_smem[kind], (CUstream)c->stream, params, nullptr));
   return MUSR_OK;
 }
 
 constexpr int kTableMax = 4096;          // c32 chi2: {err, 1/err} table entries (64 KB)
-constexpr double kCompactMax = 8388608.0;  // c32 format: counts are integers < 2^23
+constexpr double kCompactMax = 2147483648.0;  // c32 format: counts are integers < 2^31
 
 // Deepest TMA pipeline (<= max_stages) whose shared memory fits one CTA per SM:
 // `stage` bytes per stage plus `extra` (table, staged rows); `per_stage`
@@ -504,7 +508,7 @@ int plan_launch(musr_ctx* c) {
     size_t extra_rows = 0;
     if (c->n_local <= kMaxStaged) extra_rows = (size_t)c->n_local * (c->n_uniform + 2) * sizeof(double);
     int occ = 0;
-    const int st = fit_stages(c->fn[kind][c->fmt], threads, stage, 0, extra + extra_rows, max_st,
+    const int st = fit_stages(c->fn[kind][kfmt(c, kind)], threads, stage, 0, extra + extra_rows, max_st,
                               &c->dyn_smem[kind], &occ);
     if (st < 1) return set_err(c, MUSR_ERR_CUDA, "objective kernel does not fit on an SM");
     c->stages_used[kind] = st;
@@ -514,7 +518,7 @@ int plan_launch(musr_ctx* c) {
     // nodes take the place of the staged rows (musr_kernel.cuh: s_tn)
     const size_t tn_block = (size_t)MUSR_KMAX * c->cwarps * 33 * sizeof(double);  // [KMAX][TN_K * 33]
     int occ_b = 0;
-    const int st_b = fit_stages(c->fn_batch[kind][c->fmt], threads, stage, tn_block, extra, max_st,
+    const int st_b = fit_stages(c->fn_batch[kind][kfmt(c, kind)], threads, stage, tn_block, extra, max_st,
                                 &c->dyn_smem_batch[kind], &occ_b);
     c->stages_batch[kind] = st_b;
     // 0: the batched kernel does not fit (musr_eval_batch then evaluates the
@@ -565,7 +569,7 @@ int build_graphs(musr_ctx* c) {
                                 1, 0, (CUstream)c->stream, params, nullptr);
       cudaEventRecordWithFlags(c->kev[kind][0], c->stream, cudaEventRecordExternal);
       if (lr == CUDA_SUCCESS)
-        lr = g_drv.LaunchKernel(c->fn[kind][c->fmt], c->grid[kind], 1, 1, 32 * (c->cwarps + 1), 1, 1,
+        lr = g_drv.LaunchKernel(c->fn[kind][kfmt(c, kind)], c->grid[kind], 1, 1, 32 * (c->cwarps + 1), 1, 1,
                                 (unsigned)c->dyn_smem[kind], (CUstream)c->stream, params,
                                 nullptr);
       cudaEventRecordWithFlags(c->kev[kind][1], c->stream, cudaEventRecordExternal);
@@ -622,8 +626,11 @@ int open_common(int device, musr_ctx** out, musr_ctx** made) {
   }
   if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(6, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_MIN_BLOCKS")) c->min_blocks = std::max(1, std::min(4, std::atoi(v)));
-  if (const char* v = std::getenv("MUSR_CWARPS")) c->cwarps = std::atoi(v) == 8 ? 8 : 16;
-  if (c->cwarps == 16) c->min_blocks = std::min(c->min_blocks, 1);  // 544 threads: one CTA per SM
+  if (const char* v = std::getenv("MUSR_CWARPS")) {
+    const int w = std::atoi(v);
+    c->cwarps = (w == 8 || w == 32) ? w : 16;
+  }
+  if (c->cwarps >= 16) c->min_blocks = std::min(c->min_blocks, 1);  // >= 544 threads: one CTA per SM
   ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   for (auto& pair : c->kev)
     for (auto& ev : pair)
@@ -912,11 +919,15 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][1], c->mod, "musr_chi2_c32"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][0], c->mod, "musr_mlh_f64"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][1], c->mod, "musr_mlh_c32"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][2], c->mod, "musr_chi2_c32big"));
+  c->fn[1][2] = c->fn[1][1];
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_utab, c->mod, "musr_uniform_table"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][0], c->mod, "musr_chi2_f64_batch"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][1], c->mod, "musr_chi2_c32_batch"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][0], c->mod, "musr_mlh_f64_batch"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][1], c->mod, "musr_mlh_c32_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][2], c->mod, "musr_chi2_c32big_batch"));
+  c->fn_batch[1][2] = c->fn_batch[1][1];
   c->have_theory = true;
   return build_graphs(c);
 }
@@ -979,8 +990,8 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
     if (maps[i] < 0)
       return set_err(c, MUSR_ERR_ARG, "negative map entry");
 
-  // Format: c32 when every in-range count is an integer in [0, 2^23) (exact in
-  // fp32); the chi2 table covers counts below min(max count + 1, 4096) rounded
+  // Format: c32 when every in-range count is an integer in [0, 2^31) (exact in
+  // int32); the chi2 table covers counts below min(max count + 1, 4096) rounded
   // up to a power of two, larger counts get err and 1/err in-kernel.
   double max_count = 0.0;
   bool compact = n_local > 0;
@@ -1384,7 +1395,7 @@ int musr_eval_batch(musr_ctx* c, int kind, const double* p, int n_points, int n_
       const unsigned rows = (unsigned)(K * c->n_local);
       CU_TRY(c, g_drv.LaunchKernel(c->fn_utab, (rows + 3) / 4, 1, 1, 128, 1, 1, 0,
                                    (CUstream)c->stream, params, nullptr));  // a warp per row
-      CU_TRY(c, g_drv.LaunchKernel(c->fn_batch[kind][c->fmt], c->grid_batch[kind], 1, 1,
+      CU_TRY(c, g_drv.LaunchKernel(c->fn_batch[kind][kfmt(c, kind)], c->grid_batch[kind], 1, 1,
                                    32 * (c->cwarps + 1), 1, 1, (unsigned)c->dyn_smem_batch[kind],
                                    (CUstream)c->stream, params, nullptr));
     }

@@ -32,7 +32,7 @@ struct MusrHist {
 };
 
 struct MusrArgs {
-  const void* d;              // counts, packed tiles (fp64, or fp32 in the c32 format)
+  const void* d;              // counts, packed tiles (fp64, or int32 in the c32 format)
   const double* env;          // exp(-t / tau_mu), packed tiles
   const double2* table;       // c32 chi2: {max(1, sqrt(k)), 1 / that} for k < table_size
   const int* tile_hist;       // tile -> local histogram
@@ -62,7 +62,7 @@ struct MusrArgs {
   int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
   int h_inline;               // 1: hin/min/fin hold all datasets' metadata
   int stages;                 // TMA pipeline depth of this launch (<= MUSR_STAGES)
-  int big_counts;             // c32 chi2: some count >= table_size (err, 1/err computed in-kernel)
+  int pad_;
   double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)
   // Small-problem metadata inline in the kernel parameters: they arrive with
   // the launch, so the CTA prologue issues no dependent global/constant misses.

@@ -144,7 +144,7 @@ def test_tree_bitwise_across_pipeline_depth_and_tile_order(monkeypatch):
 
 def _hi_datasets(lengths, n0, seed, fractional=False):
     """Histograms whose early bins carry counts far beyond the 4096-entry
-    {err, 1/err} table (n0 up to ~8e6, still < 2^23), so one tile mixes table
+    {err, 1/err} table (n0 up to 3e7, int32 counts), so one tile mixes table
     lookups and in-kernel sqrt / reciprocal; ``fractional`` adds non-integer
     counts (the f64 format)."""
     rng = np.random.default_rng(seed)
@@ -163,7 +163,7 @@ def _hi_datasets(lengths, n0, seed, fractional=False):
     return dss
 
 
-@pytest.mark.parametrize("n0,fractional,fmt", [(1e5, False, "c32"), (8.0e6, False, "c32"),
+@pytest.mark.parametrize("n0,fractional,fmt", [(1e5, False, "c32"), (3.0e7, False, "c32"),
                                               (3000.0, True, "f64"), (1e5, True, "f64")])
 def test_chi2_tree_bitwise_count_formats(n0, fractional, fmt):
     """Counts beyond the table (err and 1/err computed per bin with the
@@ -172,7 +172,7 @@ def test_chi2_tree_bitwise_count_formats(n0, fractional, fmt):
     total; MLH within 1e-14."""
     expr = pkg.parse(THEORIES[0])
     rng = np.random.default_rng(int(n0) % 1000 + fractional)
-    dss = _hi_datasets([4095, 4097, 70001, 1, 300000], n0, seed=21 + fractional)
+    dss = _hi_datasets([4095, 4097, 70001, 1, 300000], n0, seed=21 + fractional, fractional=fractional)
     p = _params(rng)
     p[2] = n0
     got = pkg.chi2(dss, expr, p)
@@ -187,9 +187,7 @@ def test_chi2_tree_bitwise_count_formats(n0, fractional, fmt):
 def test_high_statistics_c2_theory_matches_oracle():
     """The C2 theory (Gaussian-relaxed TF precession) on N0 = 1e5 data: ~70 % of
     the bins beyond the count table; chi2 and MLH within 1e-14."""
-    w = workloads.c2(n_hist=4, nbins=1 << 16)
-    for j in range(4):
-        w.params[3 + 3 * j + 1] = 1e5
+    w = workloads.c2h(n_hist=4, nbins=1 << 16)
     dss = workloads.synthesize(w)
     sess_fmt = None
     for kind, fn, ofn in (("chi2", pkg.chi2, O.chi2), ("mlh", pkg.mlh, O.mlh)):
