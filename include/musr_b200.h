@@ -214,7 +214,7 @@ int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, 
                     double* kernel_ms);
 
 /* Data format chosen at upload: 0 = f64 (counts + envelope as fp64, 16 B/bin;
- * chi2 computes err and 1/err per bin), 1 = c32 (integral counts < 2^31: int32
+ * chi2 computes err and 1/err per bin), 1 = c32 (integral counts < 2^23: fp32
  * counts + fp64 envelope, 12 B/bin, with a {err, 1/err} table of `table_size`
  * (<= 4096) entries in shared memory; larger counts computed per bin). */
 int musr_format(const musr_ctx* ctx, int* format, int* table_size);

@@ -356,9 +356,29 @@ class _VecEmitter:
         if node.name == "exp":
             if self.uniform_of(arg):  # cannot happen: uniform calls are hoisted
                 raise TheoryError("uniform exp reached the vector emitter")
-            x = "t" if isinstance(arg, TimeVar) else self.vec(arg)
-            self.lines.append(f"  {name}[0] = musr_exp_fast({x}[0], ok);")
-            self._loop(name, f"musr_exp_anchored({x}[j], {x}[0], {name}[0], ok)", first=1)
+            # exp(c * y) with c = +-2^k (the -0.5 of sg / stg): anchored on y with the
+            # series coefficients scaled by c^k -- bit-identical, no per-bin multiply
+            scaled = _pow2_scaled(arg, self.uniform_of)
+            c, y = scaled if scaled is not None else (1.0, arg)
+            yv = "t" if isinstance(y, TimeVar) else self.vec(y)
+            x0 = f"{yv}[0]" if c == 1.0 else f"__dmul_rn({_lit(c)}, {yv}[0])"
+            k = int(math.log2(abs(c)))
+            b = [c ** 4 * float.fromhex("0x1.5555555555555p-5"),
+                 c ** 3 * float.fromhex("0x1.5555555555555p-3"), c * c * 0.5, c]
+            hi10, hi13 = (1023 - 10 - k) << 20, (1023 - 13 - k) << 20
+            dd, hm = self._fresh(), self._fresh()
+            self.lines.append(f"  {name}[0] = musr_exp_fast({x0}, ok);")
+            self.lines.append(f"  double {dd}[MUSR_PT]; int {hm} = 0;")
+            self.lines.append(f"  #pragma unroll")
+            self.lines.append(f"  for (int j = 1; j < MUSR_PT; ++j) {{ {dd}[j] = __dsub_rn({yv}[j], {yv}[0]); "
+                              f"{hm} = max({hm}, musr_hiabs({dd}[j])); }}")
+            self.lines.append(f"  ok = ok && {hm} < {hi10:#x};  // |d| < 2^-10 (d = c * dy)")
+            self.lines.append(f"  if (MUSR_EXP_DEG3 && {hm} < {hi13:#x}) {{  // |d| < 2^-13: degree 3")
+            self._loop(name, f"musr_exp_series3({dd}[j], {name}[0], {_lit(b[1])}, {_lit(b[2])}, {_lit(b[3])})",
+                       first=1)
+            self.lines.append("  } else {")
+            self._loop(name, f"musr_exp_series4({dd}[j], {name}[0], {', '.join(_lit(x) for x in b)})", first=1)
+            self.lines.append("  }")
         elif node.name in ("cos", "sin") and self.rotations is not None and arg in self.rotations:
             self._rotated(name, node.name, arg, self.rotations[arg])
         elif node.name in ("cos", "sin"):
@@ -423,6 +443,21 @@ class _VecEmitter:
         self.lines.append(f"    {name}[0] = p0_;")
         self.lines.append(f"    #pragma unroll")
         self.lines.append(f"    for (int j = 1; j < MUSR_PT; ++j) {name}[j] = musr_pow_anchored({self.ref(base, 'j')}, an_, ok); }}")
+
+
+def _pow2_scaled(arg: Node, uniform) -> Optional[Tuple[float, Node]]:
+    """(c, y) when ``arg`` is ``c * y`` or ``y * c`` with c a literal +-2^k
+    (|k| <= 8, so the scaled series coefficients stay normal) and y per-bin."""
+    if not (isinstance(arg, Binary) and arg.op == "*"):
+        return None
+    for lit, y in ((arg.left, arg.right), (arg.right, arg.left)):
+        if isinstance(lit, Num) and not uniform(y):
+            c = float(lit.value)
+            if c != 0.0 and math.isfinite(c):
+                m, e = math.frexp(abs(c))
+                if m == 0.5 and -8 <= e - 1 <= 8:
+                    return c, y
+    return None
 
 
 ROT_TABLE = 15  # bins per run a rotation table covers (MUSR_PT <= ROT_TABLE + 1)

@@ -5,7 +5,7 @@
 //     source hash (the paper's runtime kernel generation);
 //   * device layout: per-dataset in-range segments packed into aligned
 //     4096-term tiles, 16-byte-group transposed; formats c32 (integer counts
-//     < 2^31 as int32 + fp64 envelope, {err, 1/err} from a count-indexed table,
+//     < 2^23 as fp32 + fp64 envelope, {err, 1/err} from a count-indexed table,
 //     in-kernel beyond it) and f64 (counts and envelope as fp64, err and 1/err
 //     in-kernel) -- musr_layout.h, musr_kernel.cuh;
 //   * the direct path (one GPU, the default): one launch of the persistent
@@ -197,12 +197,12 @@ struct musr_ctx {
   int n_global = 0, n_local = 0;
   int64_t n_tiles = 0;
   int p_capacity = 0;
-  void* d = nullptr;            // fp64, or int32 (c32 format)
+  void* d = nullptr;            // fp64, or fp32 (c32 format, exact integers)
   double* env = nullptr;
   double2* table = nullptr;
   int table_size = 0;
   bool big_counts = false;      // c32: some count >= table_size
-  int fmt = 0;                  // 0: f64 streams, 1: c32 (int32 counts + err/rcp table)
+  int fmt = 0;                  // 0: f64 streams, 1: c32 (fp32 counts + err/rcp table)
   int* tile_hist = nullptr;
   MusrHist* hist = nullptr;
   double* P = nullptr;
@@ -255,7 +255,7 @@ struct musr_ctx {
 // Tile layout of one stream (musr_kernel.cuh): tiles of cthreads*pt terms; inside
 // a tile the 16-byte group k*cthreads + t holds thread t's elements g*k .. g*k+g-1
 // (g = 16 / element size), so consumer reads are conflict-free LDS.128.
-// mode 0: fp64 copy, 1: int32 (the c32 format: integer counts < 2^31).
+// mode 0: fp64 copy, 1: fp32 (the c32 format: integer counts < 2^23, exact).
 __global__ void musr_layout_stream(const double* __restrict__ src, void* __restrict__ dst,
                                    size_t terms, unsigned pt, unsigned cthreads, int mode) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -267,7 +267,7 @@ __global__ void musr_layout_stream(const double* __restrict__ src, void* __restr
   const unsigned grp = r / g, e = r - grp * g, k = grp / cthreads, t = grp % cthreads;
   const double v = src[tile * tile_terms + (size_t)t * pt + g * k + e];
   if (mode == 1)
-    static_cast<int*>(dst)[i] = (int)v;
+    static_cast<float*>(dst)[i] = (float)v;
   else
     static_cast<double*>(dst)[i] = v;
 }
@@ -461,7 +461,7 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
 }
 
 constexpr int kTableMax = 4096;          // c32 chi2: {err, 1/err} table entries (64 KB)
-constexpr double kCompactMax = 2147483648.0;  // c32 format: counts are integers < 2^31
+constexpr double kCompactMax = 8388608.0;  // c32 format: counts are integers < 2^23 (fp32-exact table index)
 
 // Deepest TMA pipeline (<= max_stages) whose shared memory fits one CTA per SM:
 // `stage` bytes per stage plus `extra` (table, staged rows); `per_stage`
@@ -928,6 +928,11 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][1], c->mod, "musr_mlh_c32_batch"));
   CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][2], c->mod, "musr_chi2_c32big_batch"));
   c->fn_batch[1][2] = c->fn_batch[1][1];
+  {  // the MLH kernels' exponent-folded log table, once per module (stream-ordered)
+    CUfunction init = nullptr;
+    CU_TRY(c, g_drv.ModuleGetFunction(&init, c->mod, "musr_logk_init"));
+    CU_TRY(c, g_drv.LaunchKernel(init, 8, 1, 1, 128, 1, 1, 0, (CUstream)c->stream, nullptr, nullptr));
+  }
   c->have_theory = true;
   return build_graphs(c);
 }
@@ -990,8 +995,8 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
     if (maps[i] < 0)
       return set_err(c, MUSR_ERR_ARG, "negative map entry");
 
-  // Format: c32 when every in-range count is an integer in [0, 2^31) (exact in
-  // int32); the chi2 table covers counts below min(max count + 1, 4096) rounded
+  // Format: c32 when every in-range count is an integer in [0, 2^23) (exact in
+  // fp32, and its table index by the 2^23 bias); the chi2 table covers counts below min(max count + 1, 4096) rounded
   // up to a power of two, larger counts get err and 1/err in-kernel.
   double max_count = 0.0;
   bool compact = n_local > 0;

@@ -32,7 +32,7 @@ struct MusrHist {
 };
 
 struct MusrArgs {
-  const void* d;              // counts, packed tiles (fp64, or int32 in the c32 format)
+  const void* d;              // counts, packed tiles (fp64, or fp32 in the c32 format)
   const double* env;          // exp(-t / tau_mu), packed tiles
   const double2* table;       // c32 chi2: {max(1, sqrt(k)), 1 / that} for k < table_size
   const int* tile_hist;       // tile -> local histogram

@@ -8,6 +8,9 @@
 #ifndef MUSR_PT
 #define MUSR_PT 8  // bins per consumer thread (musr_theory_vec works on one run)
 #endif
+#ifndef MUSR_EXP_DEG3
+#define MUSR_EXP_DEG3 1  // anchored exp: degree-3 series for runs with every |d| < 2^-13
+#endif
 
 __device__ __forceinline__ double musr_sq(double x) { return __dmul_rn(x, x); }
 

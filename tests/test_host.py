@@ -108,6 +108,35 @@ def test_anchored_exp_within_two_ulp(mathlib):
     assert np.isnan(far).all()  # outside the window: the kernel recomputes exactly
 
 
+def test_scaled_anchored_exp_bitwise(mathlib):
+    """exp(c * y) anchored on y with c^k-scaled coefficients (codegen's form for
+    the -0.5 of sg / stg) is bit-identical to the anchored exp of x = c * y,
+    including the window test."""
+    rng = np.random.default_rng(8)
+    n = 300_000
+    c = rng.choice([-0.5, 0.5, -2.0, 4.0, -0.25, -1.0], n)
+    y0 = rng.uniform(-300, 300, n) / np.abs(c)
+    y = y0 + rng.uniform(-2.0**-9, 2.0**-9, n) * rng.choice([1.0, 1e-2, 1e-6], n) / np.abs(c)
+    got = mathlib("v_exp_anchored_k", y, y0, c)
+    want = mathlib("v_exp_anchored", c * y, c * y0)
+    assert np.isnan(got).sum() == np.isnan(want).sum() > 0
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+def test_log_exponent_table_bitwise(mathlib):
+    """musr_log_fast_k (exponent folded into a 1024-entry table, the MLH hot
+    path) equals musr_log_fast bit for bit on [0.043, 22) and hands everything
+    else (k outside [-4, 4), zero, negative, subnormal, inf, NaN) to the exact path."""
+    rng = np.random.default_rng(9)
+    x = np.concatenate([np.exp(rng.uniform(np.log(0.6875 / 16), np.log(1.375 * 8), 400_000)),
+                        1.0 + rng.uniform(-0.05, 0.05, 100_000), [1.0, 0.6875 / 16, 1.375 * 8 * (1 - 2**-52)]])
+    got, want = mathlib("v_log_k", x), mathlib("v_log", x)
+    assert not np.isnan(got).any()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+    out = np.array([0.6875 / 16 * (1 - 2**-52), 1.375 * 8, 100.0, 1e-3, 0.0, -1.0, 5e-324, np.inf, np.nan])
+    assert np.isnan(mathlib("v_log_k", out)).all()
+
+
 def test_pow_anchor_within_two_ulp(mathlib):
     """musr_pow_fast (the anchored pow's anchor: exp(b log x) carried in
     extended precision) against libm pow; musr_rcp_approx to 1 ulp."""

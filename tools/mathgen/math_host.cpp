@@ -16,6 +16,20 @@ void v_exp_anchored(const double* x, const double* x0, double* y, long n) {
     if (!ok) y[i] = NAN;
   }
 }
+// exp(c * y) anchored on y (c = +-2^k): coefficients scaled as codegen.py emits them
+void v_exp_anchored_k(const double* y, const double* y0, const double* c, double* out, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    const double k = c[i];
+    const double e0 = musr_exp(k * y0[i]);
+    int ex;
+    frexp(fabs(k), &ex);
+    const int hi = (1023 - 10 - (ex - 1)) << 20;
+    out[i] = musr_exp_anchored_k(y[i], y0[i], e0, k * k * k * k * 0x1.5555555555555p-5,
+                                 k * k * k * 0x1.5555555555555p-3, k * k * 0.5, k, hi, ok);
+    if (!ok) out[i] = NAN;
+  }
+}
 void v_pow_anchored(const double* x, const double* x0, const double* b, double* y, long n) {
   for (long i = 0; i < n; ++i) {
     bool ok = true;
@@ -57,6 +71,17 @@ void v_log(const double* x, double* y, long n) {
   for (long i = 0; i < n; ++i) {
     bool ok = true;
     y[i] = musr_log_fast(x[i], musr_log_t, ok);
+    if (!ok) y[i] = NAN;
+  }
+}
+// the exponent-folded table log (MLH hot path), table built like the kernel's
+void v_log_k(const double* x, double* y, long n) {
+  static double2 t2[MUSR_LOGK_N];
+  static double t1[MUSR_LOGK_N];
+  for (int i = 0; i < MUSR_LOGK_N; ++i) musr_logk_entry(musr_log_t, i, &t2[i], &t1[i]);
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    y[i] = musr_log_fast_k(x[i], t2, t1, ok);
     if (!ok) y[i] = NAN;
   }
 }

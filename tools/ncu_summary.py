@@ -79,6 +79,14 @@ def main():
         for k in WANT:
             if k in d:
                 lines.append(f"{k:78s} {d[k][0]:>18s} {d[k][1]}")
+        # every per-pipe utilisation the capture holds (XU = MUFU / conversions,
+        # FP64, FMA, ALU, LSU, ...): the roofline's "which unit is busy" evidence
+        pipes = {k: num(d, k) for k in d
+                 if (k.startswith("sm__inst_executed_pipe_") or k.startswith("sm__pipe_"))
+                 and k.endswith("pct_of_peak_sustained_active")}
+        s["pipes_pct"] = pipes
+        for k in sorted(pipes):
+            lines.append(f"{k:78s} {d[k][0]:>18s} {d[k][1]}")
         for st, v in stalls.items():
             lines.append(f"{'stall_' + st + ' (per issue)':78s} {v:18.3f}")
         lines.append("# derived")
