@@ -163,8 +163,9 @@ def _hi_datasets(lengths, n0, seed, fractional=False):
     return dss
 
 
-@pytest.mark.parametrize("n0,fractional,fmt", [(1e5, False, "c32"), (3.0e7, False, "c32"),
-                                              (3000.0, True, "f64"), (1e5, True, "f64")])
+@pytest.mark.parametrize("n0,fractional,fmt", [(1e5, False, "c32"), (8.0e6, False, "c32"),
+                                              (3.0e7, False, "f64"), (3000.0, True, "f64"),
+                                              (1e5, True, "f64")])
 def test_chi2_tree_bitwise_count_formats(n0, fractional, fmt):
     """Counts beyond the table (err and 1/err computed per bin with the
     correctly rounded sqrt / reciprocal) and non-integer counts (f64 format,
@@ -182,6 +183,25 @@ def test_chi2_tree_bitwise_count_formats(n0, fractional, fmt):
     assert _bits(sess.per_dataset()) == _bits(want_per)
     assert got.hex() == float(want).hex()
     assert rel(pkg.mlh(dss, expr, p), O.mlh(dss, expr, p)) <= TOL
+
+
+@pytest.mark.parametrize("offset", [0.0, 0.5])
+def test_every_integer_count_err_rcp(offset):
+    """Every integer count in [0, 2^23) (the whole c32 domain; offset 0.5: the
+    f64 format) in one shuffled histogram: err = max(1, sqrt(d)) and 1/err come
+    from the table below its size and from the branch-free musr_sqrt_fast /
+    musr_div_fast beyond it; chi2 of a transcendental-free theory must equal the
+    oracle bit for bit."""
+    n = 1 << 23
+    rng = np.random.default_rng(23)
+    counts = rng.permutation(n).astype(np.float64) + offset
+    ds = pkg.MusrDataset(0, counts, 1e-6, 0, pkg.TheoryBinding(map=(0, 1)), 2, 3)
+    expr = pkg.parse(THEORIES[0])
+    p = np.array([0.01, -0.02, 4.0e6, 5.0])
+    got = pkg.chi2([ds], expr, p)
+    sess = objective.session_for([ds], expr, pkg.TAU_MU_US, len(p), pkg.DeviceBackend())
+    assert sess.data_format() == ("c32" if offset == 0.0 else "f64")
+    assert got.hex() == float(O.chi2([ds], expr, p)).hex()
 
 
 def test_high_statistics_c2_theory_matches_oracle():

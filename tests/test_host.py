@@ -137,6 +137,19 @@ def test_log_exponent_table_bitwise(mathlib):
     assert np.isnan(mathlib("v_log_k", out)).all()
 
 
+def test_err_rcp_fast_every_integer_count(tmp_path_factory, mathlib):
+    """The chi2 kernel's in-kernel error path (branch-free sqrt and reciprocal,
+    used for counts beyond its table and for the f64 format) equals IEEE
+    max(1, sqrt(k)) and 1/err for every integer k in [1, 2^23)."""
+    lib = C.CDLL(str(next(tmp_path_factory.getbasetemp().glob("math*")) / "libmath_host.so"))
+    lib.v_err_rcp_scan.restype = C.c_long
+    assert lib.v_err_rcp_scan(C.c_long(1), C.c_long(1 << 23)) == 0
+    rng = np.random.default_rng(12)
+    x = np.concatenate([np.exp(rng.uniform(0.0, 36.0, 500_000)), 1.0 + rng.uniform(0, 1, 100_000)])
+    assert np.array_equal(mathlib("v_sqrt_fast", x), np.sqrt(x))
+    assert np.isnan(mathlib("v_sqrt_fast", np.array([0.5, 0.0, -4.0, 2.0**53, np.inf, np.nan]))).all()
+
+
 def test_pow_anchor_within_two_ulp(mathlib):
     """musr_pow_fast (the anchored pow's anchor: exp(b log x) carried in
     extended precision) against libm pow; musr_rcp_approx to 1 ulp."""

@@ -93,4 +93,28 @@ void v_div_fast(const double* a, const double* b, double* q, long n) {
   }
 }
 
+// chi2 error and reciprocal for integer counts k in [lo, hi) by the kernel's
+// big-count path: err = max(1, musr_sqrt_fast(k)), rcp = musr_div_fast(1, err);
+// returns the number of k where either differs from IEEE (sqrt, 1 / err) or ok dropped
+long v_err_rcp_scan(long lo, long hi) {
+  long bad = 0;
+  for (long k = lo; k < hi; ++k) {
+    bool ok = true;
+    const double d = (double)k;
+    const double s = musr_sqrt_fast(d, ok);
+    const double err = s < 1.0 ? 1.0 : s;
+    const double rcp = musr_div_fast(1.0, err, ok);
+    const double e_ref = fmax(1.0, sqrt(d));
+    if (!ok || err != e_ref || rcp != 1.0 / e_ref) ++bad;
+  }
+  return bad;
+}
+void v_sqrt_fast(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool ok = true;
+    y[i] = musr_sqrt_fast(x[i], ok);
+    if (!ok) y[i] = NAN;
+  }
+}
+
 }  // extern "C"
