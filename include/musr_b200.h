@@ -213,6 +213,20 @@ int musr_nm_run(int n, const double* x0, double f0, const double* step, const do
 int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, double* ms,
                     double* kernel_ms);
 
+/* The theory's uniform row as a host program (codegen.py: _UniformProgram;
+ * int32 quadruples (op, dst, a, b) and literals), set after musr_set_theory.
+ * On the direct path with <= 16 local datasets the library then evaluates every
+ * dataset's parameter-only values, rotation tables, N0 and Nbkg on the host per
+ * call -- as the reference evaluates them as numpy float64 scalars on the CPU
+ * (theory.py:409-464, musr.py:150-162) -- and passes them inline with the launch,
+ * so the CTA prologue only copies them.  Optional: without it the prologue
+ * computes the rows on the device. */
+int musr_set_uniform_program(musr_ctx* ctx, const int32_t* code, int n_words, const double* lits,
+                              int n_lits);
+
+/* The rows the host program gives for p ([n_local][row length], test hook). */
+int musr_eval_uniform_rows(musr_ctx* ctx, const double* p, int n_p, double* rows);
+
 /* Data format chosen at upload: 0 = f64 (counts + envelope as fp64, 16 B/bin;
  * chi2 computes err and 1/err per bin), 1 = c32 (integral counts < 2^23: fp32
  * counts + fp64 envelope, 12 B/bin, with a {err, 1/err} table of `table_size`

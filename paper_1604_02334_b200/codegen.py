@@ -42,7 +42,7 @@ the reference would.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
 from .theory import (
@@ -85,6 +85,10 @@ class Lowered:
     per_bin: bool               # does A depend on t at all
     n_uniform_reg: int = 1      # MUSR_NU_REG: leading row entries kept in registers
     n_rotations: int = 0        # MUSR_NROT: rotated cos/sin arguments
+    # the uniform row as a host program (musr_set_uniform_program): int32
+    # quadruples (op, dst, a, b) over a register file, and its literals
+    uniform_code: List[int] = field(default_factory=list)
+    uniform_lits: List[float] = field(default_factory=list)
 
 
 # -- static events + literal folding on the user AST --------------------------
@@ -460,6 +464,80 @@ def _pow2_scaled(arg: Node, uniform) -> Optional[Tuple[float, Node]]:
     return None
 
 
+# Opcodes of the host uniform program (csrc/musr_b200.cu: eval_uniform_row).  Each
+# mirrors the device prologue's operation (_Emitter) with IEEE double arithmetic;
+# exp / log / cos / sin / pow are the host libm's, as numpy's float64 scalars use.
+UOP = {"LIT": 0, "P": 1, "F": 2, "NEG": 3, "ADD": 4, "SUB": 5, "MUL": 6, "DIV": 7, "SQ": 8,
+       "SQRT": 9, "RCP": 10, "POWU": 11, "POW": 12, "EXP": 13, "LOG": 14, "COS": 15, "SIN": 16,
+       "OUT": 17, "ROT": 18}
+_UOP_BIN = {"+": "ADD", "-": "SUB", "*": "MUL", "/": "DIV"}
+_UOP_CALL = {"exp": "EXP", "log": "LOG", "cos": "COS", "sin": "SIN", "sqrt": "SQRT"}
+
+
+class _UniformProgram:
+    """The uniform prologue (U slots and rotation-table slopes) as a register
+    program the host library evaluates per call; same CSE and operation choice
+    as the device emitter, so arithmetic-only rows are bit-identical to it."""
+
+    def __init__(self):
+        self.code: List[int] = []
+        self.lits: List[float] = []
+        self.regs: Dict[Node, int] = {}
+        self.n = 0
+
+    def _emit(self, op: str, a: int = 0, b: int = 0) -> int:
+        dst = self.n
+        self.n += 1
+        self.code += [UOP[op], dst, a, b]
+        return dst
+
+    def lit(self, v: float) -> int:
+        self.lits.append(float(v))
+        return self._emit("LIT", len(self.lits) - 1)
+
+    def reg(self, node: Node) -> int:
+        if isinstance(node, Num):
+            return self.lit(float(node.value))
+        if node in self.regs:
+            return self.regs[node]
+        if isinstance(node, SlotRef):
+            r = self._emit("P" if node.array == "p" else "F", node.slot)
+        elif isinstance(node, Unary):
+            r = self._emit("NEG", self.reg(node.operand))
+        elif isinstance(node, Binary) and node.op != "^":
+            r = self._emit(_UOP_BIN[node.op], self.reg(node.left), self.reg(node.right))
+        elif isinstance(node, Binary):
+            base, ex = self.reg(node.left), node.right
+            if isinstance(ex, Num):
+                e = float(ex.value)
+                if e == 2.0:
+                    r = self._emit("SQ", base)
+                elif e == 0.5:
+                    r = self._emit("SQRT", base)
+                elif e == -1.0:
+                    r = self._emit("RCP", base)
+                elif e == 1.0:
+                    r = base
+                elif e == 0.0:
+                    r = self.lit(1.0)
+                else:
+                    r = self._emit("POW", base, self.lit(e))
+            else:
+                r = self._emit("POWU", base, self.reg(ex))
+        elif isinstance(node, Call):
+            r = self._emit(_UOP_CALL[node.name], self.reg(node.args[0]))
+        else:
+            raise TheoryError(f"internal: {node!r} in a uniform subtree")
+        self.regs[node] = r
+        return r
+
+    def out(self, slot: int, node: Node) -> None:
+        self.code += [UOP["OUT"], slot, self.reg(node), 0]
+
+    def rot(self, r: int, slope: Node) -> None:
+        self.code += [UOP["ROT"], r, self.reg(slope), 0]
+
+
 ROT_TABLE = 15  # bins per run a rotation table covers (MUSR_PT <= ROT_TABLE + 1)
 
 
@@ -559,6 +637,13 @@ def lower(ast: Node, rotate: bool = True) -> Lowered:
         u_lines.extend(ue.lines)
         u_lines.append(f"  U[{i}] = {val};")
     nu_reg = max(len(order), 1)
+    uprog = _UniformProgram()
+    for i, n in enumerate(order):
+        uprog.out(i, n)
+    if not order:
+        uprog.code += [UOP["OUT"], 0, uprog.lit(0.0), 0]
+    for r, w in enumerate(slopes):
+        uprog.rot(r, w)
     rot_lines: List[str] = []
     for r, w in enumerate(slopes):   # rotation table entry j: D_j = W*(j*dt), cos D_j, sin D_j
         wv = _lit(float(w.value)) if isinstance(w, Num) else f"U[{hoisted[w]}]"
@@ -664,6 +749,8 @@ def lower(ast: Node, rotate: bool = True) -> Lowered:
         max_p_slot=max(p_slots, default=-1),
         max_f_slot=max(f_slots, default=-1),
         per_bin=per_bin,
+        uniform_code=uprog.code,
+        uniform_lits=uprog.lits,
     )
 
 

@@ -174,6 +174,12 @@ struct musr_ctx {
   CUfunction fn_batch[2][3] = {};  // musr_eval_batch
   bool have_theory = false;
   int n_uniform = 1;            // MUSR_NU of the loaded theory
+  int nu_reg = 1, n_rot = 0;    // its MUSR_NU_REG, MUSR_NROT
+  // host uniform program (musr_set_uniform_program): int32 (op, dst, a, b) + literals
+  std::vector<int32_t> ucode;
+  std::vector<double> ulits;
+  int u_nreg = 0;
+  bool device_rows = false;     // MUSR_DEVICE_ROWS (at open): rows in the CTA prologue always
   int sms = 0;                  // multiprocessors on the device
   int per_thread = 8;           // MUSR_PT: terms per consumer thread
   int cwarps = 16;              // MUSR_CWARPS: consumer warps per CTA; tile = 32*cwarps*per_thread
@@ -233,6 +239,7 @@ struct musr_ctx {
   unsigned long long epoch_base = 0;
   unsigned long long epoch = 0;
   bool direct_args_ok = false;
+  bool direct_args_rows = false;  // direct_args.u holds host rows (not pin / min / fin)
   bool h_inline = false;        // metadata small enough for kernel-parameter space
   std::vector<MusrHist> hist_host;
   std::vector<int32_t> maps_host;
@@ -407,8 +414,10 @@ MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   if (c->h_inline) {
     for (int i = 0; i < c->n_local; ++i) {
       a.hin[i] = c->hist_host[i];
-      for (int k = 0; k < c->map_stride; ++k) a.min[i][k] = c->maps_host[(size_t)i * c->map_stride + k];
-      for (int k = 0; k < c->f_stride; ++k) a.fin[i][k] = c->fvals_host[(size_t)i * c->f_stride + k];
+      for (int k = 0; k < c->map_stride; ++k)
+        a.u.dev.min[i][k] = c->maps_host[(size_t)i * c->map_stride + k];
+      for (int k = 0; k < c->f_stride; ++k)
+        a.u.dev.fin[i][k] = c->fvals_host[(size_t)i * c->f_stride + k];
     }
   }
   a.ll = c->ll_dev;
@@ -423,6 +432,94 @@ MusrArgs make_args(const musr_ctx* c, bool direct = false) {
   return a;
 }
 
+// Host uniform rows (the reference evaluates these parameter-only values as numpy
+// float64 scalars on the host, theory.py:409-464): direct path, inline metadata,
+// and all local rows within MUSR_R_INLINE doubles.
+bool host_rows_ok(const musr_ctx* c) {
+  return !c->device_rows && !c->ucode.empty() && c->h_inline && direct_mode(c) &&
+         (size_t)c->n_local * (size_t)(c->n_uniform + 2) <= MUSR_R_INLINE;
+}
+
+// Evaluate every local dataset's row [U (nu_reg) | rotation tables | N0 | Nbkg]
+// with the theory's uniform program (codegen.py: _UniformProgram) -- the same
+// operations as the device prologue (musr_uniform / musr_rot_entry) in IEEE double
+// arithmetic, exp / log / cos / sin / pow from the host libm.
+int eval_uniform_rows(const musr_ctx* c, const double* p, int n_p, double* rows) {
+  const int row = c->n_uniform + 2, pt = c->per_thread;
+  static thread_local std::vector<double> R, last_w;
+  R.assign((size_t)std::max(c->u_nreg, 1), 0.0);
+  last_w.assign((size_t)std::max(c->n_rot, 1), 0.0);
+  const int32_t* code = c->ucode.data();
+  const int n_ins = (int)c->ucode.size() / 4;
+  for (int i = 0; i < c->n_local; ++i) {
+    const int32_t* M = c->maps_host.data() + (size_t)i * c->map_stride;
+    const double* F = c->fvals_host.data() + (size_t)i * c->f_stride;
+    const MusrHist& H = c->hist_host[i];
+    double* U = rows + (size_t)i * row;
+    std::fill(U, U + row, 0.0);
+    for (int k = 0; k < n_ins; ++k) {
+      const int op = code[4 * k], d = code[4 * k + 1], x = code[4 * k + 2], y = code[4 * k + 3];
+      switch (op) {
+        case 0: R[d] = c->ulits[x]; break;
+        case 1:
+          if (x >= c->map_stride || M[x] >= n_p)
+            return set_err(const_cast<musr_ctx*>(c), MUSR_ERR_ARG, "p[m[k]] out of range");
+          R[d] = p[M[x]];
+          break;
+        case 2:
+          if (x >= c->map_stride || M[x] >= c->f_stride)
+            return set_err(const_cast<musr_ctx*>(c), MUSR_ERR_ARG, "f[m[k]] out of range");
+          R[d] = F[M[x]];
+          break;
+        case 3: R[d] = -R[x]; break;
+        case 4: R[d] = R[x] + R[y]; break;
+        case 5: R[d] = R[x] - R[y]; break;
+        case 6: R[d] = R[x] * R[y]; break;
+        case 7: R[d] = R[x] / R[y]; break;
+        case 8: R[d] = R[x] * R[x]; break;
+        case 9: R[d] = std::sqrt(R[x]); break;
+        case 10: R[d] = 1.0 / R[x]; break;
+        case 11: {  // np.power, bin-uniform exponent (musr_npy_pow_u)
+          const double b = R[y], v = R[x];
+          R[d] = b == 2.0 ? v * v : b == 0.5 ? std::sqrt(v) : b == -1.0 ? 1.0 / v
+               : b == 1.0 ? v : b == 0.0 ? 1.0 : std::pow(v, b);
+          break;
+        }
+        case 12: R[d] = std::pow(R[x], R[y]); break;
+        case 13: R[d] = std::exp(R[x]); break;
+        case 14: R[d] = std::log(R[x]); break;
+        case 15: R[d] = std::cos(R[x]); break;
+        case 16: R[d] = std::sin(R[x]); break;
+        case 17: U[d] = R[x]; break;
+        case 18: {  // rotation table d: D_j = W * (j * dt), cos D_j, sin D_j (musr_rot_entry)
+          const double W = R[x];
+          double* T = U + c->nu_reg + 4 * pt * d;
+          const double* prev = i ? rows + (size_t)(i - 1) * row + c->nu_reg + 4 * pt * d : nullptr;
+          if (prev && c->hist_host[i - 1].dt == H.dt && last_w[d] == W) {
+            std::memcpy(T, prev, sizeof(double) * 4 * pt);  // same slope and bin width
+            break;
+          }
+          last_w[d] = W;
+          for (int j = 1; j < pt; ++j) {
+            const double D = W * ((double)j * H.dt);
+            T[4 * j] = D;
+            T[4 * j + 1] = std::cos(D);
+            T[4 * j + 2] = std::sin(D);
+          }
+          break;
+        }
+        default: break;
+      }
+      (void)y;
+    }
+    if (H.n0_slot >= n_p || H.nbkg_slot >= n_p)
+      return set_err(const_cast<musr_ctx*>(c), MUSR_ERR_ARG, "N0 / Nbkg slot out of range");
+    U[c->n_uniform] = p[H.n0_slot];
+    U[c->n_uniform + 1] = p[H.nbkg_slot];
+  }
+  return MUSR_OK;
+}
+
 // The evaluation's kernels: [uniform table,] objective tiles.  `a` carries
 // the parameter vector inline when `pinl` is given (direct path).
 int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
@@ -431,12 +528,22 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
   MusrArgs local;
   MusrArgs* ap = &local;
   if (direct) {  // reuse the prebuilt block; only the inline parameters change per call
-    if (!c->direct_args_ok) {
+    const bool rows = host_rows_ok(c);
+    if (!c->direct_args_ok || c->direct_args_rows != rows) {
       c->direct_args = make_args(c, true);
       c->direct_args_ok = true;
+      c->direct_args_rows = rows;
     }
     ap = &c->direct_args;
     ap->p_inline = n_p >= 0 ? 1 : 0;
+    ap->r_inline = 0;
+    if (rows) {  // the uniform rows from the host program, in place of pin / min / fin
+      const int rc = eval_uniform_rows(c, c->last_p.data(), (int)c->last_p.size(), ap->u.rin);
+      if (rc != MUSR_OK) return rc;
+      ap->r_inline = 1;
+      ap->p_inline = 0;
+      n_p = -1;  // (pin shares the space)
+    }
   } else {
     local = make_args(c, false);
   }
@@ -448,7 +555,7 @@ int launch_kernels(musr_ctx* c, int kind, bool with_table, bool direct = false,
   a.stages = c->stages_used[kind];
   if (n_p >= 0) {
     a.p_inline = 1;
-    if (n_p) std::memcpy(a.pin, pinl, sizeof(double) * (size_t)n_p);
+    if (n_p) std::memcpy(a.u.dev.pin, pinl, sizeof(double) * (size_t)n_p);
   }
   void* params[] = {&a};
   with_table = with_table && c->n_local > kMaxStaged;
@@ -528,8 +635,10 @@ int plan_launch(musr_ctx* c) {
                  : (unsigned)std::max<int64_t>(1, std::min<int64_t>(c->n_tiles, (int64_t)c->sms * occ_b));
   }
   if (std::getenv("MUSR_TRACE") && !c->trace) {
-    CUDA_TRY(c, cudaMalloc(&c->trace, (size_t)c->sms * 8 * 4 * sizeof(unsigned long long)));
-    CUDA_TRY(c, cudaMemset(c->trace, 0, (size_t)c->sms * 8 * 4 * sizeof(unsigned long long)));
+    // per-CTA blocks (sms * 32 words), then [tile][3] stamps for up to 2^16 tiles
+    const size_t words = (size_t)c->sms * 32 + 3 * 65536;
+    CUDA_TRY(c, cudaMalloc(&c->trace, words * sizeof(unsigned long long)));
+    CUDA_TRY(c, cudaMemset(c->trace, 0, words * sizeof(unsigned long long)));
   }
   return MUSR_OK;
 }
@@ -624,6 +733,7 @@ int open_common(int device, musr_ctx** out, musr_ctx** made) {
     const int pt = std::atoi(v);
     c->per_thread = (pt == 4 || pt == 16) ? pt : 8;
   }
+  c->device_rows = std::getenv("MUSR_DEVICE_ROWS") != nullptr;
   if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(6, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_MIN_BLOCKS")) c->min_blocks = std::max(1, std::min(4, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_CWARPS")) {
@@ -908,6 +1018,10 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
                        log_cap, &cubin);
   if (rc != MUSR_OK) return rc;
   c->n_uniform = nu;
+  c->nu_reg = nu_reg;
+  c->n_rot = nrot;
+  c->ucode.clear();  // a new theory: its uniform program (if any) comes next
+  c->ulits.clear();
   free_graphs(c);
   if (c->mod) {
     g_drv.ModuleUnload(c->mod);
@@ -935,6 +1049,44 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
   }
   c->have_theory = true;
   return build_graphs(c);
+}
+
+int musr_set_uniform_program(musr_ctx* c, const int32_t* code, int n_words, const double* lits,
+                              int n_lits) {
+  if (!c) return set_err(c, MUSR_ERR_ARG, "NULL handle");
+  if (!c->have_theory) return set_err(c, MUSR_ERR_ARG, "set the theory before its uniform program");
+  if (n_words < 0 || n_words % 4 || (n_words && !code) || n_lits < 0 || (n_lits && !lits))
+    return set_err(c, MUSR_ERR_ARG, "uniform program: bad arguments");
+  int nreg = 0;
+  for (int k = 0; k < n_words / 4; ++k) {  // validate once: every operand defined before use
+    const int op = code[4 * k], d = code[4 * k + 1], x = code[4 * k + 2], y = code[4 * k + 3];
+    const bool bin = op == 4 || op == 5 || op == 6 || op == 7 || op == 11 || op == 12;
+    bool ok = op >= 0 && op <= 18;
+    if (op <= 16) {
+      ok = ok && d == nreg;
+      if (op == 0) ok = ok && x >= 0 && x < n_lits;
+      else if (op <= 2) ok = ok && x >= 0 && x < MUSR_M_INLINE;  // map slot (checked per row)
+      else ok = ok && x >= 0 && x < nreg && (!bin || (y >= 0 && y < nreg));
+      ++nreg;
+    } else if (op == 17) {
+      ok = ok && d >= 0 && d < c->nu_reg && x >= 0 && x < nreg;
+    } else {
+      ok = ok && d >= 0 && d < c->n_rot && x >= 0 && x < nreg;
+    }
+    if (!ok) return set_err(c, MUSR_ERR_ARG, fmt("uniform program: bad instruction %d", k));
+  }
+  c->ucode.assign(code, code + n_words);
+  c->ulits.assign(lits, lits + n_lits);
+  c->u_nreg = nreg;
+  c->direct_args_ok = false;
+  return MUSR_OK;
+}
+
+int musr_eval_uniform_rows(musr_ctx* c, const double* p, int n_p, double* rows) {
+  if (!c || (n_p && !p) || !rows) return set_err(c, MUSR_ERR_ARG, "NULL argument");
+  if (c->ucode.empty() || !c->have_data)
+    return set_err(c, MUSR_ERR_ARG, "uniform program and data must be set");
+  return eval_uniform_rows(c, p, n_p, rows);
 }
 
 int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index,
@@ -1320,6 +1472,12 @@ int musr_debug_trace(musr_ctx* c, int kind, uint64_t* out, int cap, int* n_ctas)
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   // [grid][4] basic stamps, then (if cap allows) [grid][4] prologue / first-tile stamps
   const int n = std::min<int>(cap / 4, (int)c->grid[kind]);
+  if (cap >= c->sms * 32 + 3 * (int)std::min<int64_t>(c->n_tiles, 65536)) {  // everything
+    const size_t all = (size_t)c->sms * 32 + 3 * (size_t)std::min<int64_t>(c->n_tiles, 65536);
+    CUDA_TRY(c, cudaMemcpy(out, c->trace, all * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    *n_ctas = n;
+    return MUSR_OK;
+  }
   const size_t words = (cap >= 20 * (int)c->grid[kind]) ? (size_t)20 * n
                        : (cap >= 16 * (int)c->grid[kind]) ? (size_t)16 * n
                        : (cap >= 8 * (int)c->grid[kind]) ? (size_t)8 * n : (size_t)4 * n;

@@ -13,6 +13,10 @@
 #define MUSR_H_INLINE 16
 #define MUSR_M_INLINE 12
 #define MUSR_F_INLINE 4
+// Uniform rows computed on the host (musr_set_uniform_program): up to this many
+// doubles (n_local * row length) travel inline in place of pin / min / fin, and
+// the CTA prologue only copies them (no dependent loads, no per-CTA arithmetic).
+#define MUSR_R_INLINE 320
 // Batched evaluation (musr_eval_batch): parameter vectors per objective launch.
 #define MUSR_KMAX 8
 
@@ -62,13 +66,18 @@ struct MusrArgs {
   int p_inline;               // 1: parameters are in `pin` (kernel parameter space)
   int h_inline;               // 1: hin/min/fin hold all datasets' metadata
   int stages;                 // TMA pipeline depth of this launch (<= MUSR_STAGES)
-  int pad_;
-  double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)
+  int r_inline;               // 1: `rin` holds every local dataset's uniform row (host-computed)
   // Small-problem metadata inline in the kernel parameters: they arrive with
   // the launch, so the CTA prologue issues no dependent global/constant misses.
   MusrHist hin[MUSR_H_INLINE];
-  int min[MUSR_H_INLINE][MUSR_M_INLINE];
-  double fin[MUSR_H_INLINE][MUSR_F_INLINE];
+  union {
+    struct {                  // rows computed in the CTA prologue from p, maps, f values
+      double pin[MUSR_P_INLINE];  // inline parameter vector (direct-launch path)
+      int min[MUSR_H_INLINE][MUSR_M_INLINE];
+      double fin[MUSR_H_INLINE][MUSR_F_INLINE];
+    } dev;
+    double rin[MUSR_R_INLINE];    // r_inline: [n_local][MUSR_NU + 2] rows from the host
+  } u;
 };
 
 #endif  // MUSR_LAYOUT_H

@@ -368,6 +368,13 @@ class Session:
         log = C.create_string_buffer(1 << 16)
         _lib.check(lib.musr_set_theory(handle, self.lowered.source.encode(), log, len(log)),
                    handle, "musr_set_theory")
+        # the parameter-only part as a host program: evaluated per call in C++ like the
+        # reference's numpy scalars, passed inline with the launch (small problems)
+        ucode = np.ascontiguousarray(self.lowered.uniform_code, dtype=np.int32)
+        ulits = np.ascontiguousarray(self.lowered.uniform_lits or [0.0], dtype=np.float64)
+        _lib.check(lib.musr_set_uniform_program(handle, ucode.ctypes.data, len(ucode),
+                                                ulits.ctypes.data, len(self.lowered.uniform_lits)),
+                   handle, "musr_set_uniform_program")
 
         def arr(a, ct):
             return np.ascontiguousarray(a).ctypes.data_as(C.POINTER(ct))

@@ -339,6 +339,68 @@ def test_full_size_c4_sampled_parity():
             assert rel(per[j], o) <= TOL, (kind, j, per[j], o)
 
 
+@pytest.mark.parametrize("src", ["p[m[0]] * sg(t, p[m[1]]) * tf(t, p[m[2]] + f[m[0]], 135.538809 * p[m[3]])",
+                                 "p[m[0]] * t + (p[m[1]] - p[m[3]]) / (2.5 * p[m[2]] + 1)",
+                                 "p[m[0]] * exp(-p[m[1]] * t) * cos(p[m[3]] ^ 1.5 * t) + log(p[m[2]]) * 0.01"])
+def test_host_uniform_rows_match_device_prologue(monkeypatch, src):
+    """The per-call host rows (musr_set_uniform_program: the parameter-only values,
+    rotation tables, N0, Nbkg passed inline) against the CTA prologue's device rows
+    (MUSR_DEVICE_ROWS): bit-identical objectives for arithmetic-only uniform parts,
+    within 1e-15 where exp / log / cos / sin / pow of parameters enter (host libm vs
+    device library), and both within 1e-14 of the oracle."""
+    expr = pkg.parse(src)
+    rng = np.random.default_rng(len(src))
+    dss = []
+    for j in range(5):
+        n = [4095, 70001, 1, 9000, 130001][j]
+        dt = 10.0 / max(n, 64)
+        lam = 900.0 * np.exp(-np.arange(n) * dt / 2.197019) + 10.0
+        dss.append(pkg.MusrDataset(j, rng.poisson(lam), dt, j % 3 if n > 8 else 0, pkg.TheoryBinding(
+            map=(0, 1, 2, 3), function_values=(30.0 * j,)), 4, 5))
+    p = np.array([0.2, 0.3, 4.0, 0.05, 1000.0, 10.0])
+    got = {}
+    for mode in ("host", "device"):
+        if mode == "device":
+            monkeypatch.setenv("MUSR_DEVICE_ROWS", "1")
+        objective.clear_cache()
+        got[mode] = [_gpu(k, dss, expr, p) for k in ("chi2", "mlh")]
+    arith = "exp" not in src
+    for i, kind in enumerate(("chi2", "mlh")):
+        (h, hp), (d, dp) = got["host"][i], got["device"][i]
+        if arith:
+            assert h == d and list(hp) == list(dp), kind
+        else:
+            assert rel(h, d) <= 1e-15 and max(rel(a, b) for a, b in zip(hp, dp)) <= 1e-14, kind
+        assert rel(h, _oracle(kind, dss, expr, p)[0]) <= TOL
+
+
+def test_host_uniform_rows_values():
+    """musr_eval_uniform_rows for the C2 theory: U = (A0, sigma, 2 pi k B, (phi + f) pi / 180)
+    exactly as numpy float64 scalars give them, rotation entries D_j = W (j dt) exactly
+    with cos / sin within an ulp of numpy's, then N0, Nbkg."""
+    import ctypes as C
+    w = workloads.c2(n_hist=3, nbins=4096)
+    dss = workloads.synthesize(w)
+    p = w.params
+    pkg.chi2(dss, w.expr, p)
+    sess = objective.session_for(dss, w.expr, pkg.TAU_MU_US, len(p), pkg.DeviceBackend())
+    row = sess.lowered.n_uniform_reg + 4 * 8 * sess.lowered.n_rotations + 2
+    rows = np.zeros((3, row))
+    pc = np.ascontiguousarray(p, dtype=np.float64)
+    assert sess._lib.musr_eval_uniform_rows(sess._handle, pc.ctypes.data, len(pc), rows.ctypes.data) == 0
+    f64 = np.float64
+    for j, ds in enumerate(dss):
+        m, fv = ds.binding.map, ds.binding.function_values
+        W = f64(2.0 * np.pi) * (f64(workloads.K_MHZ_PER_T) * f64(p[m[3]]))
+        assert rows[j, 0] == p[m[0]] and rows[j, 1] == p[m[1]] and rows[j, 2] == W
+        assert rows[j, 3] == ((f64(p[m[2]]) + f64(fv[m[4]])) * f64(np.pi)) / f64(180.0)
+        for k in range(1, 8):
+            D = W * (f64(k) * f64(ds.dt))
+            e = rows[j, 4 + 4 * k: 8 + 4 * k]
+            assert e[0] == D and abs(e[1] - np.cos(D)) <= 2.3e-16 and abs(e[2] - np.sin(D)) <= 2.3e-16
+        assert rows[j, -2] == p[ds.n0_slot] and rows[j, -1] == p[ds.nbkg_slot]
+
+
 def test_pipeline_depth_and_large_table_invariance(monkeypatch):
     """The TMA pipeline depth is picked at run time (the deepest that fits next
     to the count table and the staged rows): 1, 2 and 3 stages give identical
