@@ -13,7 +13,7 @@ w = W.WORKLOADS[name]()
 ds = W.synthesize(w)
 s = objective.session_for(ds, w.expr, musr.TAU_MU_US, len(w.params), objective.DeviceBackend())
 musr.chi2(ds, w.expr, w.params)
-ms = s.time_evals(0, 3, 1, 1) / 3
+ms = s.time_evals(0, 3, 1, int(os.environ.get("MUSR_FLUSH", "1"))) / 3
 nt = s.n_tiles()
 sms = _lib.device_sms(0) if hasattr(_lib, "device_sms") else 148
 cap = sms * 32 + 3 * nt
@@ -41,3 +41,12 @@ per = np.array([lat[cta == k].mean() for k in range(n.value)])
 print("slowest CTAs by mean publish->fold (CTA, SM, us, tiles):",
       [(int(k), int(smid[cta == k][0]), round(float(per[k]), 2), int((cta == k).sum()))
        for k in np.argsort(per)[-6:]])
+slow = int(np.argsort(per)[-1])
+typ = int(np.argsort(per)[len(per) // 2])
+for k, lab in ((slow, "slowest"), (typ, "typical")):
+    idx = np.flatnonzero(cta == k)
+    idx = idx[np.argsort(pub[idx])]
+    print(f"{lab} CTA {k} (SM {int(smid[idx[0]])}): tile(pub,done) " +
+          " ".join(f"{int(i)}({pub[i]:.1f},{done[i]:.1f})" for i in idx))
+s2 = a[sms * 16: sms * 20].reshape(-1, 4)
+print("stage-2 runs so far per CTA (slowest, typical):", int(s2[slow, 0]), int(s2[typ, 0]))
