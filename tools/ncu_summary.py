@@ -83,7 +83,7 @@ def main():
         # FP64, FMA, ALU, LSU, ...): the roofline's "which unit is busy" evidence
         pipes = {k: num(d, k) for k in d
                  if (k.startswith("sm__inst_executed_pipe_") or k.startswith("sm__pipe_"))
-                 and k.endswith("pct_of_peak_sustained_active")}
+                 and ".avg." in k and k.endswith("pct_of_peak_sustained_active")}
         s["pipes_pct"] = pipes
         for k in sorted(pipes):
             lines.append(f"{k:78s} {d[k][0]:>18s} {d[k][1]}")
