@@ -190,7 +190,7 @@ struct musr_ctx {
   double* utab = nullptr;       // uniform table (sized at graph build)
   size_t utab_rows = 0;
   unsigned long long* trace = nullptr;  // MUSR_TRACE=1: per-CTA timeline
-  unsigned* sched = nullptr;    // [2] dynamic tile scheduler (self-resetting)
+  unsigned* sched = nullptr;    // [2] dynamic tile scheduler: next tile, spare (self-resetting)
   unsigned grid[2] = {0, 0};    // persistent grid per kind
   size_t dyn_smem[2] = {0, 0};  // dynamic shared memory per kind
   unsigned grid_batch[2] = {0, 0};
@@ -444,7 +444,7 @@ bool host_rows_ok(const musr_ctx* c) {
 // with the theory's uniform program (codegen.py: _UniformProgram) -- the same
 // operations as the device prologue (musr_uniform / musr_rot_entry) in IEEE double
 // arithmetic, exp / log / cos / sin / pow from the host libm.
-int eval_uniform_rows(const musr_ctx* c, const double* p, int n_p, double* rows) {
+int eval_uniform_rows(musr_ctx* c, const double* p, int n_p, double* rows) {
   const int row = c->n_uniform + 2, pt = c->per_thread;
   static thread_local std::vector<double> R, last_w;
   R.assign((size_t)std::max(c->u_nreg, 1), 0.0);
@@ -463,12 +463,12 @@ int eval_uniform_rows(const musr_ctx* c, const double* p, int n_p, double* rows)
         case 0: R[d] = c->ulits[x]; break;
         case 1:
           if (x >= c->map_stride || M[x] >= n_p)
-            return set_err(const_cast<musr_ctx*>(c), MUSR_ERR_ARG, "p[m[k]] out of range");
+            return set_err(c, MUSR_ERR_ARG, "p[m[k]] out of range");
           R[d] = p[M[x]];
           break;
         case 2:
           if (x >= c->map_stride || M[x] >= c->f_stride)
-            return set_err(const_cast<musr_ctx*>(c), MUSR_ERR_ARG, "f[m[k]] out of range");
+            return set_err(c, MUSR_ERR_ARG, "f[m[k]] out of range");
           R[d] = F[M[x]];
           break;
         case 3: R[d] = -R[x]; break;
@@ -513,7 +513,7 @@ int eval_uniform_rows(const musr_ctx* c, const double* p, int n_p, double* rows)
       (void)y;
     }
     if (H.n0_slot >= n_p || H.nbkg_slot >= n_p)
-      return set_err(const_cast<musr_ctx*>(c), MUSR_ERR_ARG, "N0 / Nbkg slot out of range");
+      return set_err(c, MUSR_ERR_ARG, "N0 / Nbkg slot out of range");
     U[c->n_uniform] = p[H.n0_slot];
     U[c->n_uniform + 1] = p[H.nbkg_slot];
   }

@@ -54,7 +54,7 @@ struct MusrArgs {
   int n_tiles;                // tiles on this device
   int table_size;             // entries of `table` (c32 format)
   unsigned long long* trace;  // MUSR_TRACE builds: per-CTA %globaltimer stamps
-  unsigned int* sched;        // [2] dynamic tile scheduler: next tile, exited CTAs (self-resetting)
+  unsigned int* sched;        // [2] dynamic tile scheduler: next tile (self-resetting), spare
   // Direct path: results go to mapped host memory as "LL" words -- each
   // 32-bit half of a result travels with the evaluation's 32-bit epoch in one
   // 8-byte store ((half << 32) | epoch), so the host knows a word is current
