@@ -15,6 +15,8 @@ timeout 400 python bench.py --combine nccl > $O/${TAG}_bench_C4_chi2_nccl.json 2
 MUSR_BENCH_DEVICE=0 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
   --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 > $O/${TAG}_bench_C4_n2_samedev.json 2> $O/${TAG}_bench_n2.err
 timeout 600 python bench.py --impl reference > $O/${TAG}_bench_ref_C4.json 2> $O/${TAG}_bench_ref_C4.err
+timeout 900 python tools/shard_scaling.py > $O/${TAG}_shard_scaling.json 2> $O/${TAG}_shard_scaling.err
+timeout 1200 python tools/fit_c5.py 0 > $O/${TAG}_fit_c5.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 > $O/${TAG}_launches_bench.log 2>&1
 for spec in "C4 0 268435456" "C2 0 8388608" "C2 1 8388608" "C2H 0 8388608" "C4 1 268435456"; do
