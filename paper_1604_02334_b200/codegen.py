@@ -89,6 +89,8 @@ class Lowered:
     # quadruples (op, dst, a, b) over a register file, and its literals
     uniform_code: List[int] = field(default_factory=list)
     uniform_lits: List[float] = field(default_factory=list)
+    uniform_nodes: List[Node] = field(default_factory=list)   # the hoisted subtrees, U order
+    rotation_slopes: List[Node] = field(default_factory=list)  # W of each rotation table
 
 
 # -- static events + literal folding on the user AST --------------------------
@@ -751,6 +753,8 @@ def lower(ast: Node, rotate: bool = True) -> Lowered:
         per_bin=per_bin,
         uniform_code=uprog.code,
         uniform_lits=uprog.lits,
+        uniform_nodes=list(order),
+        rotation_slopes=list(slopes),
     )
 
 
