@@ -981,6 +981,12 @@ int jit_compile(musr_ctx* c, int per_thread, int stages, int min_blocks, int cwa
   cubin->resize(n);
   nvrtcGetCUBIN(prog, &(*cubin)[0]);
   nvrtcDestroyProgram(&prog);
+  if (const char* path = std::getenv("MUSR_DUMP_CUBIN")) {  // developer hook: the product SASS
+    if (FILE* f = std::fopen(path, "wb")) {
+      std::fwrite(cubin->data(), 1, cubin->size(), f);
+      std::fclose(f);
+    }
+  }
   std::lock_guard<std::mutex> lk(g_jit_mu);
   g_cubin_cache[key] = *cubin;
   return MUSR_OK;
