@@ -8,6 +8,7 @@ the oracle does, and raise the same exception type and message.  The
 ``exp`` of bare ``t`` (theory.py:91-98, 450-452).
 """
 
+import os
 import numpy as np
 import pytest
 
@@ -19,6 +20,8 @@ from paper_1604_02334_b200 import objective
 pytestmark = pytest.mark.gpu
 TOL = 1e-14   # "errors within 1e-9" needs <~1e-14 objective agreement
 N_CASES = 40
+# MUSR_FUZZ_SCALE=k runs k times as many cases per regime (deep runs; default 1)
+SCALE = max(1, int(os.environ.get("MUSR_FUZZ_SCALE", "1")))
 
 
 @pytest.fixture(autouse=True)
@@ -128,8 +131,8 @@ def _case(i, regime="typical"):
     return src, expr, dss, p
 
 
-CASES = [(i, "typical") for i in range(N_CASES)] + [(i, "low") for i in range(10)] + \
-        [(i, "real") for i in range(6)] + [(i, "logpow") for i in range(16)]
+CASES = [(i, "typical") for i in range(N_CASES * SCALE)] + [(i, "low") for i in range(10 * SCALE)] + \
+        [(i, "real") for i in range(6 * SCALE)] + [(i, "logpow") for i in range(16 * SCALE)]
 
 
 @pytest.mark.parametrize("i,regime", CASES)
