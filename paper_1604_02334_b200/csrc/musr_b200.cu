@@ -25,6 +25,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 #include <signal.h>
+#include <sys/stat.h>
 #include <unistd.h>
 
 #include <cerrno>
@@ -39,6 +40,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <thread>
 #include <vector>
 
 #include "../../include/musr_b200.h"
@@ -142,7 +144,8 @@ bool load_driver(std::string* err) {
 
 // ---- JIT cache ---------------------------------------------------------------
 std::mutex g_jit_mu;
-std::unordered_map<std::string, std::string> g_cubin_cache;  // source -> cubin
+std::unordered_map<std::string, std::vector<std::string>> g_cubin_cache;  // source -> per-entry cubins
+constexpr int kEntries = 10;  // musr_kernel.cuh: MUSR_ONLY = 1 .. 10
 
 uint64_t fnv1a(const std::string& s) {
   uint64_t h = 1469598103934665603ull;
@@ -168,7 +171,7 @@ struct musr_ctx {
   std::string err;
 
   // theory module
-  CUmodule mod = nullptr;
+  CUmodule mods[kEntries + 1] = {};  // per entry point (index 1..kEntries; see MUSR_ONLY)
   CUfunction fn[2][3] = {};  // [kind][kernel format: 0 f64, 1 c32, 2 c32 + counts beyond the table]
   CUfunction fn_utab = nullptr;
   CUfunction fn_batch[2][3] = {};  // musr_eval_batch
@@ -896,7 +899,8 @@ void musr_close(musr_ctx* c) {
       cudaHostUnregister(c->shared_host);
     }
   }
-  if (c->mod) g_drv.ModuleUnload(c->mod);
+  for (auto& m : c->mods)
+    if (m) g_drv.ModuleUnload(m);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   if (c->flush) cudaFree(c->flush);
   if (c->trace) cudaFree(c->trace);
@@ -914,9 +918,100 @@ const char* musr_last_error(const musr_ctx* c) { return c ? c->err.c_str() : g_e
 namespace {
 
 // NVRTC: (prelude + fragment + kernel template) -> sm_100a CUBIN, cached by source.
+// One NVRTC build of `src` with `opt_s`; the compiler log goes to *plog.
+int nvrtc_build(musr_ctx* c, const std::string& src, const std::vector<std::string>& opt_s,
+                const std::string& key, std::string* cubin, std::string* plog) {
+  std::vector<const char*> opts;
+  for (auto& o : opt_s) opts.push_back(o.c_str());
+  const char* hdr_src[] = {kMusrLayoutSrc, kMusrMathSrc, kMusrPreludeSrc, kMusrKernelSrc};
+  const char* hdr_name[] = {"musr_layout.h", "musr_math.cuh", "musr_prelude.cuh",
+                            "musr_kernel.cuh"};
+  const int n_hdr = sizeof(hdr_src) / sizeof(hdr_src[0]);
+  nvrtcProgram prog;
+  std::string pname = fmt("musr_theory_%016llx.cu", (unsigned long long)fnv1a(key));
+  nvrtcResult nr = nvrtcCreateProgram(&prog, src.c_str(), pname.c_str(), n_hdr, hdr_src, hdr_name);
+  if (nr != NVRTC_SUCCESS)
+    return set_err(c, MUSR_ERR_NVRTC, fmt("nvrtcCreateProgram: %s", nvrtcGetErrorString(nr)));
+  nr = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  plog->assign(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &(*plog)[0]);
+  if (nr != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return set_err(c, MUSR_ERR_NVRTC,
+                   fmt("NVRTC compile failed: %s\n", nvrtcGetErrorString(nr)) + *plog);
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin->resize(n);
+  nvrtcGetCUBIN(prog, &(*cubin)[0]);
+  nvrtcDestroyProgram(&prog);
+  return MUSR_OK;
+}
+
+// Spill-store bytes ptxas -v reported for entry point `fn` (-1 if absent).
+long spill_stores(const std::string& plog, const char* fn) {
+  const std::string tag = std::string("Function properties for ") + fn + "\n";
+  const size_t at = plog.find(tag);
+  if (at == std::string::npos) return -1;
+  const size_t eol = plog.find('\n', at + tag.size());
+  const std::string line = plog.substr(at + tag.size(), eol - at - tag.size());
+  const size_t k = line.find(" bytes spill stores");
+  if (k == std::string::npos) return -1;
+  size_t b = line.rfind(',', k);
+  b = (b == std::string::npos) ? 0 : b + 1;
+  return std::atol(line.substr(b, k - b).c_str());
+}
+
+// On-disk cubin cache ($MUSR_CACHE_DIR, default ~/.cache/musr_b200; MUSR_CACHE_DIR=""
+// disables it): a theory compiled once loads in milliseconds in later processes.
+std::string cache_path(const std::string& key, int k) {
+  const char* dir = std::getenv("MUSR_CACHE_DIR");
+  std::string d;
+  if (dir) {
+    d = dir;
+  } else if (const char* home = std::getenv("HOME")) {
+    d = std::string(home) + "/.cache/musr_b200";
+  }
+  if (d.empty()) return "";
+  return d + fmt("/%016llx_%02d.cubin", (unsigned long long)fnv1a(key), k);
+}
+bool cache_read(const std::string& path, std::string* out) {
+  if (path.empty()) return false;
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  std::fseek(f, 0, SEEK_END);
+  const long n = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  bool ok = n > 0;
+  if (ok) {
+    out->resize((size_t)n);
+    ok = std::fread(&(*out)[0], 1, (size_t)n, f) == (size_t)n;
+  }
+  std::fclose(f);
+  return ok;
+}
+void cache_write(const std::string& path, const std::string& data) {
+  if (path.empty()) return;
+  const size_t slash = path.rfind('/');
+  std::string dir = path.substr(0, slash);
+  for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+  const std::string tmp = path + fmt(".%d.tmp", (int)getpid());
+  if (FILE* f = std::fopen(tmp.c_str(), "wb")) {
+    const bool ok = std::fwrite(data.data(), 1, data.size(), f) == data.size();
+    std::fclose(f);
+    if (ok) std::rename(tmp.c_str(), path.c_str());
+    else std::remove(tmp.c_str());
+  }
+}
+
+// NVRTC: (prelude + fragment + kernel template) -> one sm_100a CUBIN per entry point,
+// the ten programs (-DMUSR_ONLY=k) built in parallel threads; cached by source and
+// options in memory and on disk.
 int jit_compile(musr_ctx* c, int per_thread, int stages, int min_blocks, int cwarps,
-                const char* fragment,
-                char* log, size_t log_cap, std::string* cubin) {
+                const char* fragment, char* log, size_t log_cap, std::vector<std::string>* cubins) {
   std::string src = std::string("#include \"musr_prelude.cuh\"\n// generated theory\n") + fragment +
                     "\n#include \"musr_kernel.cuh\"\n";
   std::vector<std::string> opt_s = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17",
@@ -938,57 +1033,74 @@ int jit_compile(musr_ctx* c, int per_thread, int stages, int min_blocks, int cwa
       }
     }
   }
-  std::vector<const char*> opts;
-  for (auto& o : opt_s) opts.push_back(o.c_str());
-  const int n_opts = (int)opts.size();
-  std::string key = src;
+  int nvrtc_major = 0, nvrtc_minor = 0;
+  nvrtcVersion(&nvrtc_major, &nvrtc_minor);
+  std::string key = src + fmt("\n//nvrtc %d.%d", nvrtc_major, nvrtc_minor);
   for (auto& o : opt_s) key += "\n//opt " + o;
   {
     std::lock_guard<std::mutex> lk(g_jit_mu);
     auto it = g_cubin_cache.find(key);
     if (it != g_cubin_cache.end()) {
-      *cubin = it->second;
+      *cubins = it->second;
       if (log && log_cap) log[0] = 0;
       return MUSR_OK;
     }
   }
-  const char* hdr_src[] = {kMusrLayoutSrc, kMusrMathSrc, kMusrPreludeSrc, kMusrKernelSrc};
-  const char* hdr_name[] = {"musr_layout.h", "musr_math.cuh", "musr_prelude.cuh",
-                            "musr_kernel.cuh"};
-  const int n_hdr = sizeof(hdr_src) / sizeof(hdr_src[0]);
-  nvrtcProgram prog;
-  std::string pname = fmt("musr_theory_%016llx.cu", (unsigned long long)fnv1a(key));
-  nvrtcResult nr = nvrtcCreateProgram(&prog, src.c_str(), pname.c_str(), n_hdr, hdr_src, hdr_name);
-  if (nr != NVRTC_SUCCESS)
-    return set_err(c, MUSR_ERR_NVRTC, fmt("nvrtcCreateProgram: %s", nvrtcGetErrorString(nr)));
-  nr = nvrtcCompileProgram(prog, n_opts, opts.data());
-  size_t log_size = 0;
-  nvrtcGetProgramLogSize(prog, &log_size);
-  std::string plog(log_size, '\0');
-  if (log_size) nvrtcGetProgramLog(prog, &plog[0]);
+  // The MLH c32 kernels' lean per-bin checks (MUSR_MLH_LEAN) pay off only while the
+  // theory leaves registers to spare: build with them, and if ptxas reports the
+  // kernel spilling more than 32 bytes (a register-heavy theory, e.g. C3's
+  // KT x exp + ge), build it again without (measured: C4 MLH -2.5 %, C3 MLH +11 %).
+  const bool auto_lean = key.find("MUSR_MLH_LEAN") == std::string::npos;
+  static const char* kName[kEntries + 1] = {"",
+      "musr_chi2_f64", "musr_chi2_c32", "musr_chi2_c32big", "musr_mlh_f64", "musr_mlh_c32",
+      "musr_chi2_f64_batch", "musr_chi2_c32_batch", "musr_chi2_c32big_batch", "musr_mlh_f64_batch",
+      "musr_mlh_c32_batch"};
+  cubins->assign(kEntries + 1, std::string());
+  std::vector<std::string> logs(kEntries + 1);
+  std::vector<int> rcs(kEntries + 1, MUSR_OK);
+  std::vector<std::string> errs(kEntries + 1);
+  auto build_one = [&](int k) {
+    const std::string path = cache_path(key, k);
+    if (cache_read(path, &(*cubins)[k])) return;
+    const bool lean_entry = auto_lean && (k == 5 || k == 10);  // MLH on c32 data
+    std::vector<std::string> o = opt_s;
+    o.push_back("-DMUSR_ONLY=" + std::to_string(k));
+    if (lean_entry) {
+      o.push_back("-DMUSR_MLH_LEAN=1");
+      o.push_back("--ptxas-options=-v");
+    }
+    musr_ctx scratch;  // per-thread error sink (set_err is not thread-safe on c)
+    int rc = nvrtc_build(&scratch, src, o, key, &(*cubins)[k], &logs[k]);
+    if (rc == MUSR_OK && lean_entry && spill_stores(logs[k], kName[k]) > 32) {
+      o.pop_back();
+      o.back() = "-DMUSR_MLH_LEAN=0";
+      rc = nvrtc_build(&scratch, src, o, key, &(*cubins)[k], &logs[k]);
+    }
+    rcs[k] = rc;
+    errs[k] = scratch.err;
+    if (rc == MUSR_OK) cache_write(path, (*cubins)[k]);
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k <= kEntries; ++k) pool.emplace_back(build_one, k);
+  for (auto& t : pool) t.join();
+  std::string all_logs;
+  for (int k = 1; k <= kEntries; ++k) all_logs += logs[k];
   if (log && log_cap) {
-    size_t n = std::min(log_cap - 1, plog.size());
-    std::memcpy(log, plog.data(), n);
+    size_t n = std::min(log_cap - 1, all_logs.size());
+    std::memcpy(log, all_logs.data(), n);
     log[n] = 0;
   }
-  if (nr != NVRTC_SUCCESS) {
-    nvrtcDestroyProgram(&prog);
-    return set_err(c, MUSR_ERR_NVRTC,
-                   fmt("NVRTC compile failed: %s\n", nvrtcGetErrorString(nr)) + plog);
-  }
-  size_t n = 0;
-  nvrtcGetCUBINSize(prog, &n);
-  cubin->resize(n);
-  nvrtcGetCUBIN(prog, &(*cubin)[0]);
-  nvrtcDestroyProgram(&prog);
+  for (int k = 1; k <= kEntries; ++k)
+    if (rcs[k] != MUSR_OK) return set_err(c, rcs[k], errs[k]);
   if (const char* path = std::getenv("MUSR_DUMP_CUBIN")) {  // developer hook: the product SASS
-    if (FILE* f = std::fopen(path, "wb")) {
-      std::fwrite(cubin->data(), 1, cubin->size(), f);
-      std::fclose(f);
-    }
+    for (int k = 1; k <= kEntries; ++k)
+      if (FILE* f = std::fopen(fmt("%s.%s", path, kName[k]).c_str(), "wb")) {
+        std::fwrite((*cubins)[k].data(), 1, (*cubins)[k].size(), f);
+        std::fclose(f);
+      }
   }
   std::lock_guard<std::mutex> lk(g_jit_mu);
-  g_cubin_cache[key] = *cubin;
+  g_cubin_cache[key] = *cubins;
   return MUSR_OK;
 }
 
@@ -998,10 +1110,12 @@ extern "C" {
 
 int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t* cubin_bytes) {
   if (!fragment) return set_err(nullptr, MUSR_ERR_ARG, "NULL fragment");
-  std::string cubin;
-  int rc = jit_compile(nullptr, 8, 3, 1, 16, fragment, log, log_cap, &cubin);  // the defaults
+  std::vector<std::string> cubins;
+  int rc = jit_compile(nullptr, 8, 3, 1, 16, fragment, log, log_cap, &cubins);  // the defaults
   if (rc != MUSR_OK) return rc;
-  if (cubin_bytes) *cubin_bytes = cubin.size();
+  size_t total = 0;
+  for (auto& cb : cubins) total += cb.size();
+  if (cubin_bytes) *cubin_bytes = total;
   return MUSR_OK;
 }
 
@@ -1017,11 +1131,11 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
     return set_err(c, MUSR_ERR_ARG,
                    "theory fragment must #define MUSR_NU_REG (>= 1) and MUSR_NROT (>= 0)");
   const int nu = nu_reg + 4 * c->per_thread * nrot;
-  std::string cubin;
+  std::vector<std::string> cubins;
   if (c->have_data && c->per_thread_data != c->per_thread * 100 + c->cwarps)  // layout <-> tile
     return set_err(c, MUSR_ERR_ARG, "tile size changed after upload");
   int rc = jit_compile(c, c->per_thread, c->stages, c->min_blocks, c->cwarps, fragment, log,
-                       log_cap, &cubin);
+                       log_cap, &cubins);
   if (rc != MUSR_OK) return rc;
   c->n_uniform = nu;
   c->nu_reg = nu_reg;
@@ -1029,28 +1143,29 @@ int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap
   c->ucode.clear();  // a new theory: its uniform program (if any) comes next
   c->ulits.clear();
   free_graphs(c);
-  if (c->mod) {
-    g_drv.ModuleUnload(c->mod);
-    c->mod = nullptr;
-  }
+  for (auto& m : c->mods)
+    if (m) {
+      g_drv.ModuleUnload(m);
+      m = nullptr;
+    }
   c->have_theory = false;
-  CU_TRY(c, g_drv.ModuleLoadData(&c->mod, cubin.data()));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][0], c->mod, "musr_chi2_f64"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][1], c->mod, "musr_chi2_c32"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][0], c->mod, "musr_mlh_f64"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][1], c->mod, "musr_mlh_c32"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][2], c->mod, "musr_chi2_c32big"));
+  for (int k = 1; k <= kEntries; ++k) CU_TRY(c, g_drv.ModuleLoadData(&c->mods[k], cubins[k].data()));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][0], c->mods[1], "musr_chi2_f64"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][1], c->mods[2], "musr_chi2_c32"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[0][2], c->mods[3], "musr_chi2_c32big"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][0], c->mods[4], "musr_mlh_f64"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn[1][1], c->mods[5], "musr_mlh_c32"));
   c->fn[1][2] = c->fn[1][1];
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_utab, c->mod, "musr_uniform_table"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][0], c->mod, "musr_chi2_f64_batch"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][1], c->mod, "musr_chi2_c32_batch"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][0], c->mod, "musr_mlh_f64_batch"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][1], c->mod, "musr_mlh_c32_batch"));
-  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][2], c->mod, "musr_chi2_c32big_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_utab, c->mods[1], "musr_uniform_table"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][0], c->mods[6], "musr_chi2_f64_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][1], c->mods[7], "musr_chi2_c32_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[0][2], c->mods[8], "musr_chi2_c32big_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][0], c->mods[9], "musr_mlh_f64_batch"));
+  CU_TRY(c, g_drv.ModuleGetFunction(&c->fn_batch[1][1], c->mods[10], "musr_mlh_c32_batch"));
   c->fn_batch[1][2] = c->fn_batch[1][1];
-  {  // the MLH kernels' exponent-folded log table, once per module (stream-ordered)
+  for (int k : {4, 5, 9, 10}) {  // the MLH modules' exponent-folded log tables (stream-ordered)
     CUfunction init = nullptr;
-    CU_TRY(c, g_drv.ModuleGetFunction(&init, c->mod, "musr_logk_init"));
+    CU_TRY(c, g_drv.ModuleGetFunction(&init, c->mods[k], "musr_logk_init"));
     CU_TRY(c, g_drv.LaunchKernel(init, 8, 1, 1, 128, 1, 1, 0, (CUstream)c->stream, nullptr, nullptr));
   }
   c->have_theory = true;
