@@ -122,6 +122,29 @@ def eval_raw():
     return _EVAL_RAW
 
 
+_PYFAST = None
+
+
+def pyfast():
+    """The CPython fast path of the drop-in call (csrc/musr_pyfast.c), bound to
+    this library's musr_eval.  Built next to the library by _build; missing
+    means the package was not built."""
+    global _PYFAST
+    if _PYFAST is None:
+        lib = load()
+        try:
+            from . import _pyfast as mod
+        except ImportError as exc:
+            raise MusrDeviceError(
+                f"the host extension _pyfast is missing ({exc}): build it with "
+                "`python -m paper_1604_02334_b200._build`") from exc
+        import numpy as np
+
+        mod.init(C.cast(lib.musr_eval, C.c_void_p).value, np.ndarray, np.dtype(np.float64))
+        _PYFAST = mod
+    return _PYFAST
+
+
 def nccl_library_path() -> Optional[str]:
     """Path of the torch-bundled libnccl.so.2, if installed."""
     env = os.environ.get("MUSR_NCCL_LIB")

@@ -171,12 +171,18 @@ def _device_backend(backend) -> DeviceBackend:
 
 
 def _evaluate(kind: int, datasets, expr, p, backend, constants) -> float:
+    # the same problem as the last call: validated and launched in C (musr_pyfast.c)
+    v = _obj.fast_evaluate(kind, datasets, expr, p, backend, constants)
+    if v is not None:
+        return v
     p = np.asarray(p, dtype=np.float64)
     if len(datasets) == 0:
         return 0.0
     sess = _obj.session_for(datasets, expr, float(constants.tau_mu), len(p),
                             _device_backend(backend))
-    return sess.evaluate(kind, p)
+    v = sess.evaluate(kind, p)
+    _obj.fast_remember(sess, datasets, expr, backend, constants)
+    return v
 
 
 def chi2(

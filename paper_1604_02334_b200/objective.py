@@ -526,6 +526,8 @@ class Session:
         return n.value
 
     def close(self) -> None:
+        if _lib._PYFAST is not None:
+            _lib._PYFAST.forget(self)
         _FROZEN.release(self)
         if self._handle:
             self._lib.musr_close(self._handle)
@@ -693,7 +695,27 @@ def _remember(datasets, expr, tau_mu, n_p, backend, sess) -> None:
                  mutations=DATASET_MUTATIONS[0])
 
 
+def fast_evaluate(kind, datasets, expr, p, backend, constants):
+    """The objective value when this call repeats the last remembered problem
+    (checked in C, musr_pyfast.c), else None: the caller takes session_for."""
+    return (_lib._PYFAST or _lib.pyfast()).evaluate(kind, datasets, expr, p, backend, constants)
+
+
+def fast_remember(sess, datasets, expr, backend, constants) -> bool:
+    """Remember a completed call for fast_evaluate.  Sessions with a static
+    error are not remembered (their calls raise)."""
+    pf = _lib.pyfast()
+    if sess.first_static is not None or not sess._handle:
+        pf.forget()
+        return False
+    s, b, t = sess._raw_out
+    return pf.remember(sess, datasets, expr, backend, constants, tuple(sess._frozen),
+                       sess._handle.value, sess.n_p, sess.n_global, s, b, t, sess._lock)
+
+
 def clear_cache() -> None:
+    if _lib._PYFAST is not None:
+        _lib._PYFAST.forget()
     _LAST["datasets"] = None
     with _CACHE_LOCK:
         while _CACHE:

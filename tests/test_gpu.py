@@ -201,6 +201,63 @@ def test_session_invalidation_on_mutation():
     assert rel(pkg.chi2(dss, w.expr, w.params), O.chi2(dss, w.expr, w.params)) <= TOL
 
 
+def test_fast_path_repeated_calls_and_every_invalidation():
+    """The C fast path (csrc/musr_pyfast.c) answers repeated calls; every edit
+    the reference would see on its next call (musr.py:181-232 reads the
+    datasets each time) gives the oracle's new value, bit for bit where the
+    slow path does."""
+    from paper_1604_02334_b200 import _lib
+
+    w = workloads.c2(n_hist=3, nbins=5000)
+    dss = workloads.synthesize(w)
+    p = np.array(w.params, dtype=np.float64)
+    cs = pkg.PhysicsConstants()
+    first = pkg.chi2(dss, w.expr, p, None, cs)          # slow path, remembered
+    assert _lib.pyfast().stats()["valid"] == 1
+    for _ in range(3):
+        assert pkg.chi2(dss, w.expr, p, None, cs) == first
+    assert rel(first, O.chi2(dss, w.expr, p)) <= TOL
+    q = p.copy()
+    q[0] *= 1.001                                       # new parameters: fast path, new value
+    assert pkg.chi2(dss, w.expr, q, None, cs) == O.chi2(dss, w.expr, q) or \
+        rel(pkg.chi2(dss, w.expr, q, None, cs), O.chi2(dss, w.expr, q)) <= TOL
+    assert pkg.mlh(dss, w.expr, q, None, cs) == pkg.mlh(dss, w.expr, q.tolist(), None, cs)
+
+    def check():
+        g = pkg.chi2(dss, w.expr, p, None, cs)
+        assert rel(g, O.chi2(dss, w.expr, p)) <= TOL
+        assert pkg.chi2(dss, w.expr, p, None, cs) == g  # and again through the fast path
+        return g
+
+    dss[1].fit_range = (0.5, 3.0)
+    a = check()
+    dss[0].dt = dss[0].dt * 1.5
+    b = check()
+    dss.pop()
+    c = check()
+    assert len({first, a, b, c}) == 4
+    dss[0].counts.flags.writeable = True                # the one way to edit in place
+    dss[0].counts[100] += 7.0
+    check()
+    dss[0].counts.flags.writeable = True                # (frozen again by the rebuild)
+    dss[0].counts[200] += 3.0
+    check()
+
+    # an MLH model that goes non-positive after a remembered call raises as the reference
+    m = pkg.parse("p[m[0]] * t")
+    ds = [pkg.MusrDataset(detector_index=4, counts=np.full(64, 5.0), dt=0.1, t0_bin=3,
+                          binding=pkg.TheoryBinding(map=(0,)), n0_slot=1, nbkg_slot=2)]
+    good = np.array([0.5, 10.0, 1.0])
+    v = pkg.mlh(ds, m, good, None, cs)
+    assert pkg.mlh(ds, m, good, None, cs) == v
+    bad = np.array([-5.0, 10.0, 1.0])
+    with pytest.raises(pkg.MusrError) as e_gpu:
+        pkg.mlh(ds, m, bad, None, cs)
+    with pytest.raises(Exception) as e_ref:
+        O.mlh(ds, m, bad)
+    assert str(e_gpu.value) == str(e_ref.value)
+
+
 # -- fits through the reference minimizer loop -----------------------------------------
 
 def _eq6_problem(n_det, nbins, seed, dt):
