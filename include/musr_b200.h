@@ -224,6 +224,14 @@ int musr_time_evals(musr_ctx* ctx, int kind, int iters, int mode, int flush_l2, 
 int musr_set_uniform_program(musr_ctx* ctx, const int32_t* code, int n_words, const double* lits,
                               int n_lits);
 
+/* Tile shape (extension, no reference counterpart): terms per consumer
+ * thread (4, 8, 16) and consumer warps per CTA (8, 16, 32); a tile is
+ * 32 * cwarps * per_thread terms.  Default 8 x 16 (4096-term tiles, the best
+ * for problems that fill the GPU); problems of a few tiles use 4 x 8 so more
+ * SMs share the work (Session picks it).  Must precede musr_set_theory and
+ * musr_upload.  The result is the same pairwise tree for every shape. */
+int musr_set_tile_shape(musr_ctx* ctx, int per_thread, int cwarps);
+
 /* The rows the host program gives for p ([n_local][row length], test hook). */
 int musr_eval_uniform_rows(musr_ctx* ctx, const double* p, int n_p, double* rows);
 

@@ -46,6 +46,7 @@ SIGNATURES = [
     ("musr_last_error", C.c_char_p, [C.c_void_p]),
     ("musr_set_theory", C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_size_t]),
     ("musr_set_uniform_program", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int]),
+    ("musr_set_tile_shape", C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     ("musr_eval_uniform_rows", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     ("musr_compile_theory", C.c_int,
      [C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),

@@ -1119,6 +1119,21 @@ int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t*
   return MUSR_OK;
 }
 
+int musr_set_tile_shape(musr_ctx* c, int per_thread, int cwarps) {
+  if (!c) return set_err(c, MUSR_ERR_ARG, "NULL handle");
+  if ((per_thread != 4 && per_thread != 8 && per_thread != 16) ||
+      (cwarps != 8 && cwarps != 16 && cwarps != 32))
+    return set_err(c, MUSR_ERR_ARG,
+                   fmt("tile shape (%d terms/thread, %d warps) not in {4,8,16} x {8,16,32}",
+                       per_thread, cwarps));
+  if (c->have_theory || c->have_data)
+    return set_err(c, MUSR_ERR_ARG, "the tile shape must be set before the theory and data");
+  c->per_thread = per_thread;
+  c->cwarps = cwarps;
+  if (c->cwarps >= 16) c->min_blocks = std::min(c->min_blocks, 1);
+  return MUSR_OK;
+}
+
 int musr_set_theory(musr_ctx* c, const char* fragment, char* log, size_t log_cap) {
   if (!c || !fragment) return set_err(c, MUSR_ERR_ARG, "NULL argument");
   CUDA_TRY(c, cudaSetDevice(c->device));

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import operator
+import os
 import threading
 from collections import OrderedDict
 from dataclasses import dataclass, field
@@ -293,6 +294,24 @@ def _fresh(exc: BaseException) -> BaseException:
 
 # -- the session ------------------------------------------------------------------------
 
+# Tile shapes (musr_set_tile_shape): 4096-term tiles (8 terms x 16 warps) fill the
+# GPU best once there are a few hundred of them; a problem of at most
+# SMALL_PROBLEM_TILES such tiles (C1: one 2^16-bin histogram = 16 tiles) leaves most
+# SMs idle and is latency-bound, so it takes 1024-term tiles (4 x 8) instead:
+# C1 chi2 13.2 -> 11.4 us per evaluation, C2 would lose 42 -> 83 us
+# (profiles/r2q_ab_tile_shape.txt).  The root is the same pairwise tree either way.
+SMALL_PROBLEM_TILES = 32
+
+
+def small_problem_tile_shape(n_terms) -> Optional[Tuple[int, int]]:
+    """(terms per thread, consumer warps) for a rank's datasets, or None for
+    the default; MUSR_PT / MUSR_CWARPS in the environment take precedence."""
+    if "MUSR_PT" in os.environ or "MUSR_CWARPS" in os.environ:
+        return None
+    tiles = sum(-(-int(n) // 4096) for n in n_terms)
+    return (4, 8) if 0 < tiles <= SMALL_PROBLEM_TILES else None
+
+
 class Session:
     """One resident objective problem (see module docstring)."""
 
@@ -365,6 +384,10 @@ class Session:
                        None, "musr_open_sharded")
         self._handle = handle
         self._lib = lib
+        shape = small_problem_tile_shape([p.n_terms for p in mine])
+        self.tile_shape = shape           # None: the library's (8 terms x 16 warps, or env)
+        if shape is not None:
+            _lib.check(lib.musr_set_tile_shape(handle, *shape), handle, "musr_set_tile_shape")
         log = C.create_string_buffer(1 << 16)
         _lib.check(lib.musr_set_theory(handle, self.lowered.source.encode(), log, len(log)),
                    handle, "musr_set_theory")

@@ -441,7 +441,8 @@ def test_host_uniform_rows_values():
     p = w.params
     pkg.chi2(dss, w.expr, p)
     sess = objective.session_for(dss, w.expr, pkg.TAU_MU_US, len(p), pkg.DeviceBackend())
-    row = sess.lowered.n_uniform_reg + 4 * 8 * sess.lowered.n_rotations + 2
+    pt = sess.tile_shape[0] if sess.tile_shape else 8          # rotation entries per thread run
+    row = sess.lowered.n_uniform_reg + 4 * pt * sess.lowered.n_rotations + 2
     rows = np.zeros((3, row))
     pc = np.ascontiguousarray(p, dtype=np.float64)
     assert sess._lib.musr_eval_uniform_rows(sess._handle, pc.ctypes.data, len(pc), rows.ctypes.data) == 0
@@ -451,7 +452,7 @@ def test_host_uniform_rows_values():
         W = f64(2.0 * np.pi) * (f64(workloads.K_MHZ_PER_T) * f64(p[m[3]]))
         assert rows[j, 0] == p[m[0]] and rows[j, 1] == p[m[1]] and rows[j, 2] == W
         assert rows[j, 3] == ((f64(p[m[2]]) + f64(fv[m[4]])) * f64(np.pi)) / f64(180.0)
-        for k in range(1, 8):
+        for k in range(1, pt):
             D = W * (f64(k) * f64(ds.dt))
             e = rows[j, 4 + 4 * k: 8 + 4 * k]
             assert e[0] == D and abs(e[1] - np.cos(D)) <= 2.3e-16 and abs(e[2] - np.sin(D)) <= 2.3e-16

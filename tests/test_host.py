@@ -592,3 +592,18 @@ def test_session_cache_freezes_counts_and_rebuilds_after_unfreeze(stub_sessions)
     objective.session_for([a], expr, 2.197019, 3, be)
     objective.session_for([b], expr, 2.197019, 4, be)
     assert not shared.flags.writeable
+
+
+def test_small_problem_tile_shape(monkeypatch):
+    """Few-tile problems take 1024-term tiles (musr_set_tile_shape 4 x 8);
+    everything else keeps the default; explicit MUSR_PT / MUSR_CWARPS win."""
+    monkeypatch.delenv("MUSR_PT", raising=False)
+    monkeypatch.delenv("MUSR_CWARPS", raising=False)
+    assert objective.small_problem_tile_shape([1 << 16]) == (4, 8)          # C1: 16 tiles
+    assert objective.small_problem_tile_shape([4096] * 32) == (4, 8)
+    assert objective.small_problem_tile_shape([4097] * 16) == (4, 8)       # 2 tiles each
+    assert objective.small_problem_tile_shape([4097] * 17) is None          # 34 tiles
+    assert objective.small_problem_tile_shape([1 << 20] * 8) is None        # C2
+    assert objective.small_problem_tile_shape([]) is None                   # rank without data
+    monkeypatch.setenv("MUSR_PT", "8")
+    assert objective.small_problem_tile_shape([1 << 16]) is None
