@@ -295,11 +295,13 @@ def _fresh(exc: BaseException) -> BaseException:
 # -- the session ------------------------------------------------------------------------
 
 # Tile shapes (musr_set_tile_shape): 4096-term tiles (8 terms x 16 warps) fill the
-# GPU best once there are a few hundred of them; a problem of at most
-# SMALL_PROBLEM_TILES such tiles (C1: one 2^16-bin histogram = 16 tiles) leaves most
-# SMs idle and is latency-bound, so it takes 1024-term tiles (4 x 8) instead:
-# C1 chi2 13.2 -> 11.4 us per evaluation, C2 would lose 42 -> 83 us
-# (profiles/r2q_ab_tile_shape.txt).  The root is the same pairwise tree either way.
+# GPU best from ~128 of them on; a problem of at most SMALL_PROBLEM_TILES such
+# tiles (C1: one 2^16-bin histogram = 16 tiles) leaves most SMs idle and is
+# latency-bound, so it takes 1024-term tiles (4 x 8): C1 chi2 13.2 -> 11.4 us,
+# 8 x 2^14 bins 18.9 -> 13.0 us; up to twice that, 2048-term tiles (4 x 16):
+# 2^18 bins 13.2 -> 12.2 us; at 128 tiles and beyond the default wins (C2: 4 x 8
+# would take 83 us instead of 42; profiles/r2q_ab_tile_shape*.txt).  The root is
+# the same pairwise tree for every shape.
 SMALL_PROBLEM_TILES = 32
 
 
@@ -309,7 +311,11 @@ def small_problem_tile_shape(n_terms) -> Optional[Tuple[int, int]]:
     if "MUSR_PT" in os.environ or "MUSR_CWARPS" in os.environ:
         return None
     tiles = sum(-(-int(n) // 4096) for n in n_terms)
-    return (4, 8) if 0 < tiles <= SMALL_PROBLEM_TILES else None
+    if tiles <= 0:
+        return None
+    if tiles <= SMALL_PROBLEM_TILES:
+        return (4, 8)
+    return (4, 16) if tiles <= 2 * SMALL_PROBLEM_TILES else None
 
 
 class Session:

@@ -602,7 +602,9 @@ def test_small_problem_tile_shape(monkeypatch):
     assert objective.small_problem_tile_shape([1 << 16]) == (4, 8)          # C1: 16 tiles
     assert objective.small_problem_tile_shape([4096] * 32) == (4, 8)
     assert objective.small_problem_tile_shape([4097] * 16) == (4, 8)       # 2 tiles each
-    assert objective.small_problem_tile_shape([4097] * 17) is None          # 34 tiles
+    assert objective.small_problem_tile_shape([4097] * 17) == (4, 16)       # 34 tiles
+    assert objective.small_problem_tile_shape([1 << 18]) == (4, 16)         # 64 tiles
+    assert objective.small_problem_tile_shape([(1 << 18) + 1]) is None      # 65 tiles
     assert objective.small_problem_tile_shape([1 << 20] * 8) is None        # C2
     assert objective.small_problem_tile_shape([]) is None                   # rank without data
     monkeypatch.setenv("MUSR_PT", "8")

@@ -9,8 +9,9 @@ from oracle import musr_oracle as O
 variants = sys.argv[1].split(";") if len(sys.argv) > 1 else [""]
 names = sys.argv[2].split(",") if len(sys.argv) > 2 else ["C2"]
 data = {}
-for n in names:
-    w = W.WORKLOADS[n]()
+for n in names:  # "C1@262144": the workload at another bin count
+    base, _, nb = n.partition("@")
+    w = W.WORKLOADS[base](nbins=int(nb)) if nb else W.WORKLOADS[base]()
     data[n] = (w, W.synthesize(w))
 ref = {}
 for v in variants:
