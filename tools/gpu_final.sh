@@ -19,7 +19,7 @@ timeout 900 python tools/shard_scaling.py > $O/${TAG}_shard_scaling.json 2> $O/$
 timeout 1200 python tools/fit_c5.py 0 > $O/${TAG}_fit_c5.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 > $O/${TAG}_launches_bench.log 2>&1
-for spec in "C4 0 268435456" "C2 0 8388608" "C2 1 8388608" "C2H 0 8388608" "C4 1 268435456"; do
+for spec in "C4 0 268435456" "C2 0 8388608" "C2 1 8388608" "C2H 0 8388608" "C4 1 268435456" "C3 0 16777216" "C3 1 16777216" "C1 0 65536"; do
   set -- $spec
   k=$([ $2 = 0 ] && echo chi2 || echo mlh)
   timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:musr_(chi2|mlh)_' -s 2 -c 1 \
@@ -27,6 +27,12 @@ for spec in "C4 0 268435456" "C2 0 8388608" "C2 1 8388608" "C2H 0 8388608" "C4 1
 done
 python tools/ncu_summary.py $O/${TAG}_ncu 268435456:$O/${TAG}_C4_chi2.ncu-rep 8388608:$O/${TAG}_C2_chi2.ncu-rep \
   8388608:$O/${TAG}_C2_mlh.ncu-rep 8388608:$O/${TAG}_C2H_chi2.ncu-rep 268435456:$O/${TAG}_C4_mlh.ncu-rep \
+  16777216:$O/${TAG}_C3_chi2.ncu-rep 16777216:$O/${TAG}_C3_mlh.ncu-rep 65536:$O/${TAG}_C1_chi2.ncu-rep \
   > $O/${TAG}_roofline_traffic.json 2> $O/${TAG}_ncu_summary.err
 python tools/ncu_hotspots.py $O/${TAG}_C4_chi2.ncu-rep > $O/${TAG}_ncu_C4_chi2_hotspots.txt 2>&1
-rm -f $O/${TAG}_C2*.ncu-rep $O/${TAG}_C4_mlh.ncu-rep   # keep one report (C4 chi2) under the 64 MiB merge cap
+rm -f $O/${TAG}_C2*.ncu-rep $O/${TAG}_C4_mlh.ncu-rep $O/${TAG}_C3*.ncu-rep $O/${TAG}_C1*.ncu-rep   # keep one report (C4 chi2) under the 64 MiB merge cap
+timeout 900 python -m pytest tests -m gpu -q > $O/${TAG}_gputest_tail.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.txt 2>&1
+for tool in memcheck synccheck; do
+  timeout 600 compute-sanitizer --tool $tool python tools/san_run.py small > $O/${TAG}_san_small_$tool.txt 2>&1
+done
