@@ -558,9 +558,10 @@ class Session:
         if _lib._PYFAST is not None:
             _lib._PYFAST.forget(self)
         _FROZEN.release(self)
-        if self._handle:
-            self._lib.musr_close(self._handle)
-            self._handle = None
+        with self._lock:                 # not while another thread evaluates on the handle
+            if self._handle:
+                self._lib.musr_close(self._handle)
+                self._handle = None
 
     def __del__(self):
         try:
