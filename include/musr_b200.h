@@ -227,9 +227,11 @@ int musr_set_uniform_program(musr_ctx* ctx, const int32_t* code, int n_words, co
 /* Tile shape (extension, no reference counterpart): terms per consumer
  * thread (4, 8, 16) and consumer warps per CTA (8, 16, 32); a tile is
  * 32 * cwarps * per_thread terms.  Default 8 x 16 (4096-term tiles, the best
- * for problems that fill the GPU); problems of a few tiles use 4 x 8 so more
- * SMs share the work (Session picks it).  Must precede musr_set_theory and
- * musr_upload.  The result is the same pairwise tree for every shape. */
+ * for problems that fill the GPU); problems of at most 64 such tiles use 8 x 8
+ * so more SMs share the work (Session picks it).  Must precede musr_set_theory
+ * and musr_upload.  The reduction is the same pairwise tree for every shape;
+ * with the same per_thread the values are bit-identical (the theory's anchored
+ * recurrences restart every per_thread bins). */
 int musr_set_tile_shape(musr_ctx* ctx, int per_thread, int cwarps);
 
 /* The rows the host program gives for p ([n_local][row length], test hook). */

@@ -295,14 +295,17 @@ def _fresh(exc: BaseException) -> BaseException:
 # -- the session ------------------------------------------------------------------------
 
 # Tile shapes (musr_set_tile_shape): 4096-term tiles (8 terms x 16 warps) fill the
-# GPU best from ~128 of them on; a problem of at most SMALL_PROBLEM_TILES such
+# GPU best from ~128 of them on.  A problem of at most SMALL_PROBLEM_TILES such
 # tiles (C1: one 2^16-bin histogram = 16 tiles) leaves most SMs idle and is
-# latency-bound, so it takes 1024-term tiles (4 x 8): C1 chi2 13.2 -> 11.4 us,
-# 8 x 2^14 bins 18.9 -> 13.0 us; up to twice that, 2048-term tiles (4 x 16):
-# 2^18 bins 13.2 -> 12.2 us; at 128 tiles and beyond the default wins (C2: 4 x 8
-# would take 83 us instead of 42; profiles/r2q_ab_tile_shape*.txt).  The root is
-# the same pairwise tree for every shape.
-SMALL_PROBLEM_TILES = 32
+# latency-bound, so it takes 2048-term tiles of 8 terms x 8 warps: C1 chi2
+# 13.2 -> 12.3 us, 2^17 bins 13.2 -> 11.6 us, 8 x 2^14 bins 18.9 -> 17.4 us; at 128
+# default tiles and beyond the default wins (profiles/r2q_ab_tile_shape*.txt).
+# The terms per thread stay 8, so every value -- transcendental theories
+# included -- is bit-identical to the default shape's, and a rank's choice can
+# never make a sharded run differ from the one-GPU run (4 terms per thread was
+# ~7 % faster still for C1, but moves transcendental values by an ulp: the
+# anchored recurrences restart at each thread's first bin).
+SMALL_PROBLEM_TILES = 64
 
 
 def small_problem_tile_shape(n_terms) -> Optional[Tuple[int, int]]:
@@ -311,11 +314,7 @@ def small_problem_tile_shape(n_terms) -> Optional[Tuple[int, int]]:
     if "MUSR_PT" in os.environ or "MUSR_CWARPS" in os.environ:
         return None
     tiles = sum(-(-int(n) // 4096) for n in n_terms)
-    if tiles <= 0:
-        return None
-    if tiles <= SMALL_PROBLEM_TILES:
-        return (4, 8)
-    return (4, 16) if tiles <= 2 * SMALL_PROBLEM_TILES else None
+    return (8, 8) if 0 < tiles <= SMALL_PROBLEM_TILES else None
 
 
 class Session:

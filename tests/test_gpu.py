@@ -201,6 +201,30 @@ def test_session_invalidation_on_mutation():
     assert rel(pkg.chi2(dss, w.expr, w.params), O.chi2(dss, w.expr, w.params)) <= TOL
 
 
+def test_small_problem_tile_shape_gives_identical_bits(monkeypatch):
+    """A few-tile problem runs with 2048-term tiles (8 terms x 8 warps,
+    objective.small_problem_tile_shape); its chi2 / MLH values -- transcendental
+    theory, per dataset and total -- equal the default 4096-term shape's bit for
+    bit, so a rank's shape choice can never change a sharded result."""
+    for w in (workloads.c1(nbins=1 << 16), workloads.c2(n_hist=3, nbins=70001)):
+        dss = workloads.synthesize(w)
+        got = {}
+        for forced in (False, True):
+            objective.clear_cache()
+            if forced:
+                monkeypatch.setenv("MUSR_CWARPS", "16")          # the default shape
+            for kind in ("chi2", "mlh"):
+                total, per = _gpu(kind, dss, w.expr, w.params)
+                sess = objective.session_for(dss, w.expr, pkg.TAU_MU_US, len(w.params),
+                                             pkg.DeviceBackend())
+                assert sess.tile_shape == (None if forced else (8, 8))
+                got[(forced, kind)] = (total, list(per))
+            monkeypatch.delenv("MUSR_CWARPS", raising=False)
+        for kind in ("chi2", "mlh"):
+            assert got[(False, kind)] == got[(True, kind)], kind
+            assert rel(got[(False, kind)][0], _oracle(kind, dss, w.expr, w.params)[0]) <= TOL
+
+
 def test_fast_path_repeated_calls_and_every_invalidation():
     """The C fast path (csrc/musr_pyfast.c) answers repeated calls; every edit
     the reference would see on its next call (musr.py:181-232 reads the
