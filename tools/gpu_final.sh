@@ -33,6 +33,3 @@ python tools/ncu_hotspots.py $O/${TAG}_C4_chi2.ncu-rep > $O/${TAG}_ncu_C4_chi2_h
 rm -f $O/${TAG}_C2*.ncu-rep $O/${TAG}_C4_mlh.ncu-rep $O/${TAG}_C3*.ncu-rep $O/${TAG}_C1*.ncu-rep   # keep one report (C4 chi2) under the 64 MiB merge cap
 timeout 900 python -m pytest tests -m gpu -q > $O/${TAG}_gputest_tail.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.txt 2>&1
-for tool in memcheck synccheck; do
-  timeout 600 compute-sanitizer --tool $tool python tools/san_run.py small > $O/${TAG}_san_small_$tool.txt 2>&1
-done
