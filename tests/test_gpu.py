@@ -225,6 +225,39 @@ def test_small_problem_tile_shape_gives_identical_bits(monkeypatch):
             assert rel(got[(False, kind)][0], _oracle(kind, dss, w.expr, w.params)[0]) <= TOL
 
 
+def test_concurrent_calls_from_threads_are_serialised():
+    """Several threads calling the drop-in objective on one cached problem (the
+    C fast path and, when its lock is busy, the Python path) get exactly the
+    values of sequential calls: evaluations on a handle never interleave."""
+    import threading
+
+    w = workloads.c2(n_hist=4, nbins=40000)
+    dss = workloads.synthesize(w)
+    rng = np.random.default_rng(21)
+    P = [w.params * (1.0 + 0.02 * rng.standard_normal(len(w.params))) for _ in range(24)]
+    want = [(pkg.chi2(dss, w.expr, p), pkg.mlh(dss, w.expr, p)) for p in P]
+    got = {}
+    errors = []
+
+    def worker(k):
+        try:
+            for rep in range(5):
+                for i in range(k, len(P), 4):
+                    got[(k, rep, i)] = (pkg.chi2(dss, w.expr, P[i]), pkg.mlh(dss, w.expr, P[i]))
+        except BaseException as exc:        # pragma: no cover - reported below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert len(got) == 5 * len(P)
+    for (k, rep, i), v in got.items():
+        assert v == want[i], (k, rep, i)
+
+
 def test_fast_path_repeated_calls_and_every_invalidation():
     """The C fast path (csrc/musr_pyfast.c) answers repeated calls; every edit
     the reference would see on its next call (musr.py:181-232 reads the
