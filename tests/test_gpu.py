@@ -570,10 +570,13 @@ def _shared_rank(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_shared_host_results_two_ranks_match_one_gpu(tmp_path):
-    """Two ranks (processes) on this GPU, each owning half the datasets, combine
-    their results through the shared host buffer: every rank gets the one-GPU
-    values bit for bit, batched calls and the MLH error included."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_shared_host_results_two_ranks_match_one_gpu(tmp_path, world):
+    """Two (four) ranks -- processes -- on this GPU, each owning a contiguous
+    share of the datasets, combine their results through the shared host
+    buffer: every rank gets the one-GPU values bit for bit, batched calls and
+    the MLH error included.  (No rank's kernel waits on another's: only the
+    hosts poll the buffer, so sharing one GPU cannot deadlock.)"""
     import socket
 
     import torch.multiprocessing as mp
@@ -581,7 +584,7 @@ def test_shared_host_results_two_ranks_match_one_gpu(tmp_path):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    mp.spawn(_shared_rank, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_shared_rank, args=(world, port, str(tmp_path)), nprocs=world, join=True)
     w = workloads.c2(n_hist=7, nbins=1 << 16)
     dss = workloads.synthesize(w)
     rng = np.random.default_rng(3)
@@ -599,7 +602,7 @@ def test_shared_host_results_two_ranks_match_one_gpu(tmp_path):
     import pickle
 
     want = [[float(v) for v in x] if not isinstance(x, str) else x for x in want]
-    for r in range(2):
+    for r in range(world):
         with open(tmp_path / f"rank{r}.pkl", "rb") as f:
             assert pickle.load(f) == want, r
 
