@@ -225,7 +225,7 @@ int musr_set_uniform_program(musr_ctx* ctx, const int32_t* code, int n_words, co
                               int n_lits);
 
 /* Tile shape (extension, no reference counterpart): terms per consumer
- * thread (4, 8, 16) and consumer warps per CTA (8, 16, 32); a tile is
+ * thread (4, 8, 16) and consumer warps per CTA (8, 16); a tile is
  * 32 * cwarps * per_thread terms.  Default 8 x 16 (4096-term tiles, the best
  * for problems that fill the GPU); problems of at most 64 such tiles use 8 x 8
  * so more SMs share the work (Session picks it).  Must precede musr_set_theory
