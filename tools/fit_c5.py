@@ -64,9 +64,11 @@ out.update(gpu_fit_s=t_gpu, gpu_evals=gpu.objective_evaluations, gpu_iterations=
 pstart = pkg.ParameterSet(values=start.values.copy(), names=list(start.names),
                           step_sizes=start.step_sizes.copy(), bounds=list(start.bounds),
                           fixed=start.fixed.copy())
+pkg.chi2(dss, expr, w.params)          # session build outside (as for the reference's loop)
 t0 = time.perf_counter()
 own = pkg.minimize("chi2", dss, expr, pstart)
 out.update(pkg_minimize_fit_s=time.perf_counter() - t0,
+           pkg_minimize_evals=own.objective_evaluations,
            pkg_minimize_bitwise_equal=bool(np.array_equal(own.best_parameters.values,
                                                           gpu.best_parameters.values)
                                            and own.objective_value == gpu.objective_value))
