@@ -15,9 +15,14 @@ resident on one GPU (or one shard of it on one rank).  Building a session:
    for this parameter-vector length (empty range, map coverage / range,
    literal division by zero, N0/Nbkg index) in the reference's order.
 
-An evaluation copies p to pinned memory and replays the CUDA graph
-(``musr_eval``); the host only folds the per-dataset sums in dataset order
-and maps the first failing dataset to the reference exception.
+An evaluation (``musr_eval``) launches the objective kernel once with p and
+the host-evaluated uniform rows inside the kernel parameters (one GPU; the
+sharded NCCL path replays a CUDA graph instead) and reads the per-dataset
+results as they land in mapped host memory; the host folds them in dataset
+order and maps the first failing dataset to the reference exception.  A call
+that repeats the last completed problem is validated and launched in C
+(``fast_evaluate``, csrc/musr_pyfast.c); anything else comes through
+``session_for``.
 """
 
 from __future__ import annotations
