@@ -737,7 +737,8 @@ int open_common(int device, musr_ctx** out, musr_ctx** made) {
     c->per_thread = (pt == 4 || pt == 16) ? pt : 8;
   }
   c->device_rows = std::getenv("MUSR_DEVICE_ROWS") != nullptr;
-  if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(6, std::atoi(v)));
+  // (5+ stages overflow the 48 KB static shared memory of the f64 MLH entry point)
+  if (const char* v = std::getenv("MUSR_STAGES")) c->stages = std::max(1, std::min(4, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_MIN_BLOCKS")) c->min_blocks = std::max(1, std::min(4, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_CWARPS")) {
     const int w = std::atoi(v);
