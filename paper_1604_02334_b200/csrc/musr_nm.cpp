@@ -16,6 +16,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -54,9 +55,21 @@ struct NmResult {
 
 // The core.  `fail_x` receives the point whose evaluation reported a nonzero
 // status (the caller re-raises there).  Returns that status or MUSR_OK.
+// `speculate`: evaluate the reflection, expansion and both contraction points
+// of an iteration as one batch before deciding (their coordinates depend only
+// on the simplex), then take the values the sequential algorithm asks for.
+// Every point's value equals its single evaluation bit for bit, and `calls`
+// counts only the points the sequential loop evaluates, so iterates, counts
+// and budget are unchanged; a failing batch (a speculative point the loop
+// might never evaluate) falls back to the sequential evaluations, which fail
+// exactly where the reference does.  Opt-in (MUSR_NM_SPECULATE=1): measured
+// slower, because a batched evaluation takes the graph path (p upload, uniform
+// table kernel, objective, D2H) -- C1 fit 6.4 -> 9.0 ms, C2 152 -> 356 ms
+// (profiles/r2q_ab_nm_speculate.txt) -- while one point is a single direct launch.
 int nm_core(int n, const double* x0, double f0, const double* step, const double* lo,
             const double* hi, double tol_f, int64_t budget, int restarts, const EvalFn& f1,
-            const EvalManyFn& fmany, double* best_x_out, NmResult* res, double* fail_x) {
+            const EvalManyFn& fmany, double* best_x_out, NmResult* res, double* fail_x,
+            bool speculate = false) {
   const double alpha = 1.0, beta = 1.0 + 2.0 / n, gamma = 0.75 - 1.0 / (2.0 * n);
   const double delta = (n > 1) ? (1.0 - 1.0 / n) : 0.5;
   int64_t calls = 1;  // the initial point (evaluated by the caller)
@@ -93,6 +106,7 @@ int nm_core(int n, const double* x0, double f0, const double* step, const double
 
   std::vector<Vec> simplex(n + 1, Vec(n));
   Vec values(n + 1);
+  Vec spec;  // speculative points, 4 x n
   std::vector<int> rank(n + 1);
   for (int pass = 0; pass < restarts + 1; ++pass) {
     simplex[0] = best_x;
@@ -140,14 +154,38 @@ int nm_core(int n, const double* x0, double f0, const double* step, const double
       Vec xr(n);
       for (int j = 0; j < n; ++j) xr[j] = c[j] + alpha * (c[j] - worst[j]);
       clamp(xr);
+      // speculative batch: [xr, xe, outside contraction, inside contraction]
+      bool spec_ok = false;
+      double sf[4];
+      if (speculate) {
+        spec.assign((size_t)4 * n, 0.0);
+        for (int j = 0; j < n; ++j) {
+          spec[j] = xr[j];
+          spec[n + j] = c[j] + beta * (xr[j] - c[j]);
+          spec[2 * n + j] = c[j] + gamma * (xr[j] - c[j]);
+          spec[3 * n + j] = c[j] - gamma * (c[j] - worst[j]);
+        }
+        for (int r = 1; r < 4; ++r)
+          for (int j = 0; j < n; ++j)
+            spec[r * n + j] = np_minimum(np_maximum(spec[r * n + j], lo[j]), hi[j]);
+        int bad_row = 0;
+        spec_ok = fmany(spec.data(), 4, sf, &bad_row) == MUSR_OK;
+      }
+      // the value at x (speculative slot `slot`, or evaluated now)
+      auto value_at = [&](int slot, const Vec& x, double* f) -> int {
+        if (!spec_ok) return eval(x, f);
+        ++calls;
+        *f = sf[slot];
+        return MUSR_OK;
+      };
       double fr;
-      if (const int rc = eval(xr, &fr)) return rc;
+      if (const int rc = value_at(0, xr, &fr)) return rc;
       if (fr < values[0]) {
         Vec xe(n);
         for (int j = 0; j < n; ++j) xe[j] = c[j] + beta * (xr[j] - c[j]);
         clamp(xe);
         double fe;
-        if (const int rc = eval(xe, &fe)) return rc;
+        if (const int rc = value_at(1, xe, &fe)) return rc;
         if (fe < fr) {
           simplex[n] = xe;
           values[n] = fe;
@@ -163,14 +201,15 @@ int nm_core(int n, const double* x0, double f0, const double* step, const double
         continue;
       }
       Vec xc(n);
-      if (fr < values[n]) {
+      const bool outside = fr < values[n];
+      if (outside) {
         for (int j = 0; j < n; ++j) xc[j] = c[j] + gamma * (xr[j] - c[j]);
       } else {
         for (int j = 0; j < n; ++j) xc[j] = c[j] - gamma * (c[j] - worst[j]);
       }
       clamp(xc);
       double fc;
-      if (const int rc = eval(xc, &fc)) return rc;
+      if (const int rc = value_at(outside ? 2 : 3, xc, &fc)) return rc;
       if (fc < py_min2(fr, values[n])) {
         simplex[n] = xc;
         values[n] = fc;
@@ -223,8 +262,9 @@ int musr_nm_run(int n, const double* x0, double f0, const double* step, const do
     return rc;
   };
   NmResult r;
+  const char* sv = std::getenv("MUSR_NM_SPECULATE");  // tests: the speculative loop on the host
   const int rc = nm_core(n, x0, f0, step, lo, hi, tol_f, budget, restarts, f1, fm, best_x, &r,
-                         fail_x);
+                         fail_x, sv && std::atoi(sv) != 0);
   if (best_f) *best_f = r.best_f;
   if (iterations) *iterations = r.iterations;
   if (evaluations) *evaluations = r.evaluations;
@@ -275,9 +315,12 @@ int musr_minimize(musr_ctx* c, int kind, const double* p_full, int n_p, const in
   int unused = 0;
   EvalFn f1 = [&](const double* x, double* f) { return eval(x, 1, f, &unused); };
   EvalManyFn fm = [&](const double* xs, int k, double* fs, int* bad_row) { return eval(xs, k, fs, bad_row); };
+  // speculative batches (see nm_core): opt-in, measured slower than single launches
+  const char* sv = std::getenv("MUSR_NM_SPECULATE");
+  const bool speculate = sv && std::atoi(sv) != 0;
   NmResult r;
   const int rc = nm_core(n_free, x0, f0, step, lo, hi, tol_f, budget, restarts, f1, fm, best_x, &r,
-                         fail_x);
+                         fail_x, speculate);
   if (best_f) *best_f = r.best_f;
   if (iterations) *iterations = r.iterations;
   if (evaluations) *evaluations = r.evaluations;

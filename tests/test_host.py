@@ -470,10 +470,15 @@ def _native_nm(fn, x0, steps, lo, hi, tol_f=1e-9, budget=0, restarts=1):
     return best, bf.value, it.value, ev.value, bool(conv.value)
 
 
+@pytest.mark.parametrize("speculate", ["0", "1"])
 @pytest.mark.parametrize("case", ["rosen2", "rosen5_bounded", "bowl_budget", "nan_region", "one_d"])
-def test_native_nelder_mead_bitwise_equal_to_python(case):
+def test_native_nelder_mead_bitwise_equal_to_python(case, speculate, monkeypatch):
     """The native loop (musr_minimize's core) reproduces optimize.nelder_mead
-    bit for bit: iterates, values, iteration and evaluation counts."""
+    bit for bit: iterates, values, iteration and evaluation counts -- also when
+    it evaluates each iteration's reflection, expansion and contraction points
+    as one speculative batch (MUSR_NM_SPECULATE=1, what musr_minimize does for
+    small problems)."""
+    monkeypatch.setenv("MUSR_NM_SPECULATE", speculate)
     from paper_1604_02334_b200.optimize import MinimizeConfig, nelder_mead
 
     rosen = lambda x: float(np.sum(100.0 * (x[1:] - x[:-1] ** 2) ** 2 + (1 - x[:-1]) ** 2))
@@ -522,6 +527,44 @@ def test_native_nelder_mead_reports_failing_point():
                          C.cast(keep, C.c_void_p), None, P(best), None, None, None, None, P(fail))
     assert rc == 100
     assert fail.tolist() == seen[4]
+
+
+def test_speculative_nelder_mead_fails_where_the_sequential_loop_fails(monkeypatch):
+    """An objective that fails on a region of parameter space: the speculative
+    loop (batched reflection / expansion / contractions) must abort at exactly
+    the point the sequential loop aborts at -- a speculative point it would
+    never have evaluated must not fail the fit -- or finish identically."""
+    lib = _lib.load()
+    CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_int,
+                     C.POINTER(C.c_double))
+
+    def cb(user, xs, k, n, fs):
+        for i in range(k):
+            x = [xs[i * n + j] for j in range(n)]
+            if x[0] > 1.6 and x[1] < -0.9:             # the "raising" region
+                return 100
+            fs[i] = (x[0] - 1.0) ** 2 + 3.0 * (x[1] + 0.5) ** 2 + 0.1 * x[0] * x[1]
+        return 0
+
+    keep = CB(cb)
+    P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    lo, hi = np.full(2, -np.inf), np.full(2, np.inf)
+    outcomes = {}
+    for start in ([0.0, 0.0], [2.0, 1.0], [-1.0, -2.0], [1.3, 0.3], [2.5, -0.5], [1.5, -0.6]):
+        for spec in ("0", "1"):
+            monkeypatch.setenv("MUSR_NM_SPECULATE", spec)
+            x0, st = np.array(start), np.array([0.5, 0.5])
+            best, fail = np.zeros(2), np.full(2, np.nan)
+            bf, it, ev = C.c_double(), C.c_int64(), C.c_int64()
+            f0 = (start[0] - 1.0) ** 2 + 3.0 * (start[1] + 0.5) ** 2 + 0.1 * start[0] * start[1]
+            rc = lib.musr_nm_run(2, P(x0), f0, P(st), P(lo), P(hi), 1e-12, 800, 1,
+                                 C.cast(keep, C.c_void_p), None, P(best), C.byref(bf),
+                                 C.byref(it), C.byref(ev), None, P(fail))
+            outcomes[(tuple(start), spec)] = (rc, fail.tobytes() if rc else best.tobytes(),
+                                              None if rc else (bf.value, it.value, ev.value))
+        assert outcomes[(tuple(start), "0")] == outcomes[(tuple(start), "1")], start
+    assert any(v[0] == 100 for v in outcomes.values())     # the region is reached somewhere
+    assert any(v[0] == 0 for v in outcomes.values())
 
 
 # -- session cache (objective.session_for) with a stand-in for the device session ----
