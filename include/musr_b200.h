@@ -225,10 +225,10 @@ int musr_set_uniform_program(musr_ctx* ctx, const int32_t* code, int n_words, co
                               int n_lits);
 
 /* Tile shape (extension, no reference counterpart): terms per consumer
- * thread (4, 8, 16) and consumer warps per CTA (8, 16); a tile is
+ * thread (4, 8, 16) and consumer warps per CTA (4, 8, 16); a tile is
  * 32 * cwarps * per_thread terms.  Default 8 x 16 (4096-term tiles, the best
  * for problems that fill the GPU); problems of at most 64 such tiles use 8 x 8
- * so more SMs share the work (Session picks it).  Must precede musr_set_theory
+ * (at most 16: 8 x 4) so more SMs share the work (Session picks it).  Must precede musr_set_theory
  * and musr_upload.  The reduction is the same pairwise tree for every shape;
  * with the same per_thread the values are bit-identical (the theory's anchored
  * recurrences restart every per_thread bins). */

@@ -742,7 +742,7 @@ int open_common(int device, musr_ctx** out, musr_ctx** made) {
   if (const char* v = std::getenv("MUSR_MIN_BLOCKS")) c->min_blocks = std::max(1, std::min(4, std::atoi(v)));
   if (const char* v = std::getenv("MUSR_CWARPS")) {
     const int w = std::atoi(v);
-    c->cwarps = (w == 8) ? 8 : 16;  // 32 + the producer would exceed 1024 threads
+    c->cwarps = (w == 4 || w == 8) ? w : 16;  // 32 + the producer would exceed 1024 threads
   }
   if (c->cwarps >= 16) c->min_blocks = std::min(c->min_blocks, 1);  // >= 544 threads: one CTA per SM
   ce = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -1123,9 +1123,10 @@ int musr_compile_theory(const char* fragment, char* log, size_t log_cap, size_t*
 int musr_set_tile_shape(musr_ctx* c, int per_thread, int cwarps) {
   if (!c) return set_err(c, MUSR_ERR_ARG, "NULL handle");
   // (32 consumer warps + the producer would exceed 1024 threads per CTA)
-  if ((per_thread != 4 && per_thread != 8 && per_thread != 16) || (cwarps != 8 && cwarps != 16))
+  if ((per_thread != 4 && per_thread != 8 && per_thread != 16) ||
+      (cwarps != 4 && cwarps != 8 && cwarps != 16))
     return set_err(c, MUSR_ERR_ARG,
-                   fmt("tile shape (%d terms/thread, %d warps) not in {4,8,16} x {8,16}",
+                   fmt("tile shape (%d terms/thread, %d warps) not in {4,8,16} x {4,8,16}",
                        per_thread, cwarps));
   if (c->have_theory || c->have_data)
     return set_err(c, MUSR_ERR_ARG, "the tile shape must be set before the theory and data");

@@ -302,9 +302,10 @@ def _fresh(exc: BaseException) -> BaseException:
 # Tile shapes (musr_set_tile_shape): 4096-term tiles (8 terms x 16 warps) fill the
 # GPU best from ~128 of them on.  A problem of at most SMALL_PROBLEM_TILES such
 # tiles (C1: one 2^16-bin histogram = 16 tiles) leaves most SMs idle and is
-# latency-bound, so it takes 2048-term tiles of 8 terms x 8 warps: C1 chi2
-# 13.2 -> 12.3 us, 2^17 bins 13.2 -> 11.6 us, 8 x 2^14 bins 18.9 -> 17.4 us; at 128
-# default tiles and beyond the default wins (profiles/r2q_ab_tile_shape*.txt).
+# latency-bound, so it takes 2048-term tiles of 8 terms x 8 warps: 2^17 bins
+# 13.2 -> 11.6 us, 8 x 2^14 bins 18.9 -> 17.4 us -- and up to 16 such tiles
+# 1024-term tiles of 8 x 4 warps: C1 chi2 13.2 -> ~11.8 us; at 128 default tiles
+# and beyond the default wins (profiles/r2q_ab_tile_shape*.txt).
 # The terms per thread stay 8, so every value -- transcendental theories
 # included -- is bit-identical to the default shape's, and a rank's choice can
 # never make a sharded run differ from the one-GPU run (4 terms per thread was
@@ -319,7 +320,9 @@ def small_problem_tile_shape(n_terms) -> Optional[Tuple[int, int]]:
     if "MUSR_PT" in os.environ or "MUSR_CWARPS" in os.environ:
         return None
     tiles = sum(-(-int(n) // 4096) for n in n_terms)
-    return (8, 8) if 0 < tiles <= SMALL_PROBLEM_TILES else None
+    if tiles <= 0 or tiles > SMALL_PROBLEM_TILES:
+        return None
+    return (8, 4) if tiles <= SMALL_PROBLEM_TILES // 4 else (8, 8)
 
 
 class Session:

@@ -202,8 +202,8 @@ def test_session_invalidation_on_mutation():
 
 
 def test_small_problem_tile_shape_gives_identical_bits(monkeypatch):
-    """A few-tile problem runs with 2048-term tiles (8 terms x 8 warps,
-    objective.small_problem_tile_shape); its chi2 / MLH values -- transcendental
+    """A few-tile problem runs with 1024- / 2048-term tiles (8 terms x 4 / 8
+    warps, objective.small_problem_tile_shape); its chi2 / MLH values -- transcendental
     theory, per dataset and total -- equal the default 4096-term shape's bit for
     bit, so a rank's shape choice can never change a sharded result."""
     for w in (workloads.c1(nbins=1 << 16), workloads.c2(n_hist=3, nbins=70001)):
@@ -217,7 +217,8 @@ def test_small_problem_tile_shape_gives_identical_bits(monkeypatch):
                 total, per = _gpu(kind, dss, w.expr, w.params)
                 sess = objective.session_for(dss, w.expr, pkg.TAU_MU_US, len(w.params),
                                              pkg.DeviceBackend())
-                assert sess.tile_shape == (None if forced else (8, 8))
+                assert sess.tile_shape == (None if forced else
+                                           ((8, 4) if len(dss) == 1 else (8, 8)))
                 got[(forced, kind)] = (total, list(per))
             monkeypatch.delenv("MUSR_CWARPS", raising=False)
         for kind in ("chi2", "mlh"):

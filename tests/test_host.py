@@ -638,13 +638,14 @@ def test_session_cache_freezes_counts_and_rebuilds_after_unfreeze(stub_sessions)
 
 
 def test_small_problem_tile_shape(monkeypatch):
-    """Few-tile problems take 2048-term tiles of 8 terms x 8 warps
+    """Few-tile problems take 1024- or 2048-term tiles of 8 terms x 4 / 8 warps
     (musr_set_tile_shape); everything else keeps the default; explicit
     MUSR_PT / MUSR_CWARPS win.  The terms per thread never change, so values
     are bit-identical for every shape (the GPU suite checks it)."""
     monkeypatch.delenv("MUSR_PT", raising=False)
     monkeypatch.delenv("MUSR_CWARPS", raising=False)
-    assert objective.small_problem_tile_shape([1 << 16]) == (8, 8)          # C1: 16 tiles
+    assert objective.small_problem_tile_shape([1 << 16]) == (8, 4)          # C1: 16 tiles
+    assert objective.small_problem_tile_shape([(1 << 16) + 1]) == (8, 8)    # 17 tiles
     assert objective.small_problem_tile_shape([4097] * 32) == (8, 8)        # 2 tiles each
     assert objective.small_problem_tile_shape([1 << 18]) == (8, 8)          # 64 tiles
     assert objective.small_problem_tile_shape([(1 << 18) + 1]) is None      # 65 tiles
