@@ -201,6 +201,32 @@ def test_session_invalidation_on_mutation():
     assert rel(pkg.chi2(dss, w.expr, w.params), O.chi2(dss, w.expr, w.params)) <= TOL
 
 
+def test_tile_shape_api_validates():
+    """musr_set_tile_shape: only {4, 8, 16} terms x {4, 8, 16} warps, and only
+    before the theory and data (the layout and the compiled kernel depend on it)."""
+    import ctypes as C
+
+    from paper_1604_02334_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.musr_set_tile_shape(None, 8, 8) != 0
+    h = C.c_void_p()
+    assert lib.musr_open(0, C.byref(h)) == 0
+    try:
+        for pt, cw in ((8, 32), (3, 8), (8, 2), (32, 8)):
+            assert lib.musr_set_tile_shape(h, pt, cw) != 0, (pt, cw)
+        assert lib.musr_set_tile_shape(h, 8, 4) == 0
+        from paper_1604_02334_b200 import codegen
+
+        frag = codegen.lower(workloads.c1(nbins=4096).expr.ast).source
+        log = C.create_string_buffer(1 << 16)
+        assert lib.musr_set_theory(h, frag.encode(), log, len(log)) == 0
+        assert lib.musr_set_tile_shape(h, 8, 8) != 0          # after the theory: refused
+        assert b"before the theory" in lib.musr_last_error(h)
+    finally:
+        lib.musr_close(h)
+
+
 def test_small_problem_tile_shape_gives_identical_bits(monkeypatch):
     """A few-tile problem runs with 1024- / 2048-term tiles (8 terms x 4 / 8
     warps, objective.small_problem_tile_shape); its chi2 / MLH values -- transcendental

@@ -41,6 +41,7 @@ def test_library_reports_no_device_cleanly():
         h = C.c_void_p()
         assert lib.musr_open(0, C.byref(h)) != 0
         assert b"device" in lib.musr_global_error().lower()
+    assert lib.musr_set_tile_shape(None, 8, 8) != 0      # NULL handle: an error, no crash
 
 
 def test_no_cpu_fallback_without_device():
