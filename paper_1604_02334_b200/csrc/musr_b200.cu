@@ -225,7 +225,10 @@ struct musr_ctx {
   double* h_p = nullptr;    // pinned
   double* P_batch = nullptr;    // [MUSR_KMAX][p_capacity] (musr_eval_batch)
   double* h_p_batch = nullptr;  // pinned staging of P_batch
-  double* h_out_batch = nullptr;  // pinned, [MUSR_KMAX][2 * n_global]
+  double* h_out_batch = nullptr;  // pinned + mapped, [MUSR_KMAX][2 * n_global]
+  double* h_out_batch_dev = nullptr;  // device alias of h_out_batch (host-row batches write here)
+  double* h_utab = nullptr;     // pinned: host-evaluated rows of a batch, [MUSR_KMAX][n_local][row]
+  size_t h_utab_rows = 0;
   double* h_out = nullptr;  // pinned + mapped, 2 * n_global
   double* h_out_dev = nullptr;  // device alias of h_out (direct path writes here)
   std::vector<double> last_p;   // parameter vector of the last evaluation (timing replays)
@@ -374,7 +377,10 @@ void free_data(musr_ctx* c) {
   c->P_batch = nullptr;
   if (c->h_p_batch) cudaFreeHost(c->h_p_batch);
   if (c->h_out_batch) cudaFreeHost(c->h_out_batch);
-  c->h_p_batch = c->h_out_batch = nullptr;
+  c->h_p_batch = c->h_out_batch = c->h_out_batch_dev = nullptr;
+  if (c->h_utab) cudaFreeHost(c->h_utab);
+  c->h_utab = nullptr;
+  c->h_utab_rows = 0;
   if (c->ll_host && c->ll_host != c->shared_host) cudaFreeHost(c->ll_host);
   c->ll_host = c->ll_dev = nullptr;
   if (c->h_p) cudaFreeHost(c->h_p);
@@ -1364,7 +1370,8 @@ int musr_upload(musr_ctx* c, int n_global, int n_local, const int32_t* out_index
       cudaHostAlloc((void**)&c->h_p_batch, (size_t)MUSR_KMAX * p_capacity * 8,
                     cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc((void**)&c->h_out_batch, (size_t)MUSR_KMAX * 2 * n_global * 8,
-                    cudaHostAllocDefault) != cudaSuccess) {
+                    cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->h_out_batch_dev, c->h_out_batch, 0) != cudaSuccess) {
     free_data(c);
     return set_err(c, MUSR_ERR_NOMEM, "pinned host allocation failed");
   }
@@ -1673,6 +1680,51 @@ int musr_eval_batch(musr_ctx* c, int kind, const double* p, int n_points, int n_
                                first_bad_bin ? first_bad_bin + (size_t)k * G : nullptr,
                                totals ? totals + k : nullptr);
       if (rc != MUSR_OK) return rc;
+    }
+    return MUSR_OK;
+  }
+  // Host rows (the single-evaluation path's rows, host_rows_ok): the batch's
+  // uniform rows are evaluated on the host like a single call's and copied in
+  // with one H2D; the kernel writes its results straight into mapped host memory.
+  // One copy + one launch + a sync instead of p upload, uniform-table kernel,
+  // objective, D2H and a sync -- and every point's rows are the very rows its
+  // single evaluation uses.
+  if (host_rows_ok(c) && c->n_tiles > 0) {
+    const size_t row = (size_t)c->n_uniform + 2, per_point = (size_t)c->n_local * row;
+    if (c->h_utab_rows < (size_t)MUSR_KMAX * per_point) {
+      if (c->h_utab) cudaFreeHost(c->h_utab);
+      c->h_utab = nullptr;
+      c->h_utab_rows = 0;
+      CUDA_TRY(c, cudaHostAlloc((void**)&c->h_utab, (size_t)MUSR_KMAX * per_point * 8,
+                                cudaHostAllocDefault));
+      c->h_utab_rows = (size_t)MUSR_KMAX * per_point;
+    }
+    for (int base = 0; base < n_points; base += MUSR_KMAX) {
+      const int K = std::min(MUSR_KMAX, n_points - base);
+      for (int k = 0; k < K; ++k)
+        if (const int rc = eval_uniform_rows(c, p + (size_t)(base + k) * n_p, n_p,
+                                             c->h_utab + (size_t)k * per_point))
+          return rc;
+      CUDA_TRY(c, cudaMemcpyAsync(c->utab, c->h_utab, (size_t)K * per_point * 8,
+                                  cudaMemcpyHostToDevice, c->stream));
+      MusrArgs a = make_args(c, false);
+      a.P = c->P_batch;  // not read: the rows carry every parameter-dependent value
+      a.p_stride = cap;
+      a.p_inline = 0;
+      a.n_points = K;
+      a.epoch = 0;
+      a.out = c->h_out_batch_dev;
+      a.stages = c->stages_batch[kind];
+      void* params[] = {&a};
+      CU_TRY(c, g_drv.LaunchKernel(c->fn_batch[kind][kfmt(c, kind)], c->grid_batch[kind], 1, 1,
+                                   32 * (c->cwarps + 1), 1, 1, (unsigned)c->dyn_smem_batch[kind],
+                                   (CUstream)c->stream, params, nullptr));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      for (int k = 0; k < K; ++k)
+        fold_results(c->h_out_batch + (size_t)k * 2 * G, G,
+                     per_dataset ? per_dataset + (size_t)(base + k) * G : nullptr,
+                     first_bad_bin ? first_bad_bin + (size_t)(base + k) * G : nullptr,
+                     totals ? totals + base + k : nullptr);
     }
     return MUSR_OK;
   }
